@@ -1,0 +1,167 @@
+/*
+ * zeus_b200.h -- C ABI of libzeus_sm100.so, the B200 (sm_100a) implementation
+ * of the reference's multistart optimizer hot path (arxiv/paper_2603_28770,
+ * "Zeus"; reference package /root/reference/pkg/src/zeus).
+ *
+ * Conventions
+ *  - Plain C types only: device pointers are raw CUDA device addresses (from
+ *    torch tensors or cudaMalloc), owned by the caller; `stream` is a
+ *    cudaStream_t passed as void*.  Every call is asynchronous on `stream`.
+ *  - Point sets are SoA, coordinate-major: coordinate k of point i is
+ *    x[k * ld + i]  (ld >= n).  This is what makes PSO loads coalesced.
+ *  - Return value: 0 on success, < 0 on error (ZEUS_ERR_*); the message is
+ *    available from zeus_last_error() on the calling host thread.  No C++
+ *    exception crosses this boundary.
+ *  - Objective ids follow the reference registry (objectives.py:145-182).
+ *  - Status codes follow bfgs.py:32-35.
+ *
+ * Each entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/pkg/src/zeus/).
+ */
+#ifndef ZEUS_B200_H
+#define ZEUS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZEUS_ABI_VERSION 1
+
+/* objective ids (objectives.py:145-182 _REGISTRY) */
+#define ZEUS_OBJ_ROSENBROCK 0
+#define ZEUS_OBJ_RASTRIGIN 1
+#define ZEUS_OBJ_ACKLEY 2
+#define ZEUS_OBJ_GOLDSTEIN_PRICE 3
+
+/* BFGS statuses (bfgs.py:32-35) */
+#define ZEUS_CONVERGED 0
+#define ZEUS_DIVERGED 1
+#define ZEUS_STOPPED 2
+#define ZEUS_DOMAIN_ERROR 3
+
+/* error codes */
+#define ZEUS_OK 0
+#define ZEUS_ERR_ARGUMENT (-1)
+#define ZEUS_ERR_CUDA (-2)
+#define ZEUS_ERR_WORKSPACE (-3)
+#define ZEUS_ERR_UNSUPPORTED (-4)
+
+/* Per-start BFGS outputs (bfgs.py:43-56 BfgsOutcome, plus work counters the
+ * roofline accounting needs).  Every pointer is a device array of n entries
+ * except x_final (SoA, [d][ld_out]).  Counters may be NULL. */
+typedef struct zeus_bfgs_out {
+  double *x_final;      /* BfgsOutcome.x_final, SoA [d][ld_out]           */
+  int64_t ld_out;
+  double *f_final;      /* BfgsOutcome.f_final (NaN if f raised)          */
+  double *grad_norm;    /* BfgsOutcome.grad_norm (+inf if none computed)  */
+  int32_t *iterations;  /* BfgsOutcome.iterations                         */
+  uint8_t *status;      /* BfgsOutcome.status (ZEUS_CONVERGED ...)        */
+  int32_t *ls_trials;   /* objective evaluations spent in line searches   */
+  int32_t *grad_evals;  /* forward-AD gradient evaluations                */
+} zeus_bfgs_out;
+
+/* BFGS / line-search hyper-parameters: bfgs_run(theta, iter_bfgs) bfgs.py:80-87,
+ * LineSearchParams linesearch.py:16-37. */
+typedef struct zeus_bfgs_params {
+  double theta;
+  int32_t iter_bfgs;
+  int32_t iter_ls;
+  double c1_armijo;
+  double alpha0;
+  double shrink;
+} zeus_bfgs_params;
+
+/* ---- library ---------------------------------------------------------- */
+int zeus_abi_version(void);
+const char *zeus_last_error(void);
+/* device properties used for persistent-grid sizing; -1 on error */
+int zeus_sm_count(int device);
+
+/* ---- counter-based streams: streams.py:21-54 (ParticleStreams.draw_uniform,
+ * numpy Philox(key=[seed, i]) + Generator.uniform).  out[r * count + c] is
+ * draw k0 + c of particle i0 + r, i.e. row-major [n][count]. */
+int zeus_philox_uniform(uint64_t seed, int64_t i0, int64_t n, uint64_t k0, int64_t count,
+                        double low, double high, double *out, void *stream);
+
+/* ---- objectives: objectives.py:33-113 (values) and autodiff.py:243-266
+ * forward_gradient.  x is SoA [d][ldx]; f[n]; grad SoA [d][ldx];
+ * domain_error[n] = 1 where the reference raises DomainError. */
+int zeus_objective_value(int obj, int d, int64_t n, const double *x, int64_t ldx,
+                         double *f, void *stream);
+int zeus_objective_gradient(int obj, int d, int64_t n, const double *x, int64_t ldx,
+                            double *grad, uint8_t *domain_error, void *stream);
+
+/* ---- PSO: pso.py:79-164.  The swarm shard is particles [i0, i0+n) of the
+ * global swarm (streams are keyed by the GLOBAL index, so any sharding gives
+ * bit-identical particles).  x, v, pbest are SoA [d][ld]; pval[n].
+ * After init / each sweep the kernel leaves this shard's best personal best
+ * in `cand` = [f, (double)global_index, x_0 .. x_{d-1}]  (d + 2 doubles).
+ * workspace: zeus_pso_workspace_bytes(n). */
+size_t zeus_pso_workspace_bytes(int64_t n);
+/* init_swarm (pso.py:79-120) */
+int zeus_pso_init(int obj, int d, int64_t n, int64_t i0, uint64_t seed, double lower,
+                  double upper, double *x, double *v, double *pbest, double *pval,
+                  int64_t ld, double *cand, void *workspace, void *stream);
+/* update_swarm (pso.py:123-164) for 0-based sweep `sweep`, reading the
+ * previous barrier's global best gX[d] (pso.py:143). */
+int zeus_pso_sweep(int obj, int d, int64_t n, int64_t i0, uint64_t seed, int sweep,
+                   double w, double c1, double c2, double *x, double *v, double *pbest,
+                   double *pval, int64_t ld, const double *gX, double *cand,
+                   void *workspace, void *stream);
+/* _reduce_global_best across shards (pso.py:73-76): cands[ncand][d+2] from
+ * every shard (e.g. an NCCL all-gather); writes the np.argmin winner to
+ * gX[d] and gbest[2] = {f, (double)global_index}. */
+int zeus_minloc_select(int d, int ncand, const double *cands, double *gX, double *gbest,
+                       void *stream);
+
+/* ---- multistart BFGS: bfgs.py:80-156 bfgs_run over n independent starts,
+ * with autodiff.py:243 gradients, linesearch.py:40 Armijo search and
+ * bfgs.py:59 inverse-Hessian update fused in one persistent kernel.
+ * x0 is SoA [d][ldx] (for zeus_run: the final swarm positions, driver.py:244).
+ * Early stop (driver.py:153-177): if `stop_counter`/`stop_flag` are non-NULL,
+ * each converged start atomically increments *stop_counter and the one that
+ * reaches `required_c` sets *stop_flag = 1; every start polls *stop_flag at
+ * the top of each iteration (bfgs.py:115-117) and ends `stopped`.
+ * workspace: zeus_bfgs_workspace_bytes(d, n). */
+size_t zeus_bfgs_workspace_bytes(int d, int64_t n);
+int zeus_bfgs(int obj, int d, int64_t n, const double *x0, int64_t ldx,
+              const zeus_bfgs_params *params, int64_t required_c,
+              unsigned long long *stop_counter, int *stop_flag, zeus_bfgs_out *out,
+              void *workspace, void *stream);
+
+/* ---- reduce_best + converged_count: driver.py:115-134, 251.  Strict '<' over
+ * starts whose status != DOMAIN_ERROR and f is not NaN, lowest index on ties.
+ * best[2] = {f, (double)(i0 + index)} or {NaN, -1} when none is valid;
+ * tallies[4] += per-status counts.  workspace: zeus_argmin_workspace_bytes(n). */
+size_t zeus_argmin_workspace_bytes(int64_t n);
+int zeus_reduce_best(int64_t n, int64_t i0, const double *f_final, const uint8_t *status,
+                     double *best, unsigned long long *tallies, void *workspace,
+                     void *stream);
+
+/* ---- building blocks exposed for the reference's public helpers --------- */
+/* armijo_search (linesearch.py:40-71) on n independent problems: x, p, g SoA
+ * [d][ld]; f0[n]; alpha[n]; trials[n] = objective evaluations used. */
+int zeus_armijo(int obj, int d, int64_t n, const double *x, const double *p,
+                const double *g, int64_t ld, const double *f0, const zeus_bfgs_params *params,
+                double *alpha, int32_t *trials, void *stream);
+/* hessian_update (bfgs.py:59-77) on n problems: H[n][d][d] row-major (in
+ * place), dx/dg [n][d]; updated[n] = 0 where the curvature guard skipped. */
+int zeus_hessian_update(int d, int64_t n, double *H, const double *dx, const double *dg,
+                        uint8_t *updated, void *stream);
+
+/* ---- measurement ------------------------------------------------------- */
+/* FP64 FMA throughput microbenchmark (the roofline denominator for the BFGS
+ * kernel; MEASURED_PEAKS.json has no FP64 figure).  Launches blocks x threads
+ * threads each running `iters` x 32 independent DFMAs; *flops_out receives
+ * the FLOP count of the launch (time it with events on `stream`).
+ * sink: device scratch of >= blocks doubles. */
+int zeus_bench_dfma(int blocks, int threads, long long iters, double *sink, double *flops_out,
+                    void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZEUS_B200_H */

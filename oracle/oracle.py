@@ -83,6 +83,13 @@ def lib():
                                         ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                         ctypes.c_int, ctypes.POINTER(Outcome), _dp]
+        L.oracle_zeus_run.restype = _i64
+        L.oracle_zeus_run.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _u64, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_int, ctypes.c_double, ctypes.c_int, _dp, _dp, _dp,
+                                      _dp, _dp, _dp, ctypes.POINTER(Outcome), _dp]
         L.oracle_reduce_best.restype = _i64
         L.oracle_reduce_best.argtypes = [ctypes.POINTER(Outcome), _i64]
         _LIB = L
@@ -198,3 +205,27 @@ def reduce_best(f_final, status) -> int:
         if best < 0 or f < f_final[best]:
             best = i
     return best
+
+
+def zeus_run(obj, d: int, n: int, seed: int, lower: float, upper: float, iter_pso: int,
+             iter_bfgs: int, theta=1e-6, threads=None, w=0.5, c1_pso=1.2, c2_pso=1.5,
+             c1_ls=0.3, alpha0=1.0, iter_ls=20, shrink=0.5):
+    """Deterministic zeus_run (driver.py:220-265, required_c = N): PSO on one
+    thread (as the reference), BFGS on a pthread pool.  Returns
+    (converged_count, best_index, pso_best, BfgsResult)."""
+    if threads is None:
+        threads = os.cpu_count() or 1
+    x = np.empty((n, d)); v = np.empty((n, d)); p = np.empty((n, d)); pv = np.empty(n)
+    gX = np.empty(d); pb = ctypes.c_double()
+    out = (Outcome * n)()
+    xf = np.empty((n, d))
+    best = lib().oracle_zeus_run(_obj(obj), d, n, seed & (2**64 - 1), lower, upper, iter_pso,
+                                 w, c1_pso, c2_pso, theta, iter_bfgs, c1_ls, alpha0, iter_ls,
+                                 shrink, threads, _p(x), _p(v), _p(p), _p(pv), _p(gX),
+                                 ctypes.byref(pb), out, _p(xf))
+    arr = np.frombuffer(out, dtype=np.dtype([(f, "f8" if f in ("f_final", "grad_norm")
+                                               else "i8") for f, _ in Outcome._fields_]))
+    res = BfgsResult(xf, arr["f_final"].copy(), arr["grad_norm"].copy(),
+                     arr["iterations"].copy(), arr["status"].copy(),
+                     arr["ls_trials"].copy(), arr["grad_evals"].copy())
+    return int(np.sum(res.status == 0)), int(best), pb.value, res

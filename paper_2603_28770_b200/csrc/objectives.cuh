@@ -1,0 +1,238 @@
+// objectives.cuh -- device objectives and lane-mapped forward-mode AD.
+//
+// Each registered objective of the reference (objectives.py:33-113) is written
+// ONCE as a template over the scalar type, mirroring the Python text operation
+// by operation, and instantiated with `double` (values) and `Dual` (tangents).
+// `Dual` reproduces autodiff.py:62-240 rule by rule (including the
+// scalar-on-the-left forms and the sqrt'(0) DomainError), and the library is
+// built with -fmad=false, so a value evaluation here is the reference's float
+// evaluation up to libm ulps (bit-exact for Rosenbrock / Goldstein-Price).
+//
+// Gradients (autodiff.py:243-266 forward_gradient seeds coordinate i and
+// re-evaluates the whole objective).  Every registered objective is a
+// sequential fold over "terms", and a term that does not touch x_i carries a
+// zero tangent, which adds exactly nothing to the fold.  So the reference's
+// tangent for coordinate i equals the fold of the tangents of the terms that
+// contain x_i -- O(1) terms instead of O(d).  Lanes own coordinates: lane i
+// seeds its own tangent and evaluates only its terms in Dual arithmetic; the
+// value sweep (real parts of shared accumulators, e.g. Ackley's two sums) is
+// computed once per start and broadcast.
+#pragma once
+#include "zeus_common.cuh"
+
+namespace zeus {
+
+// ---- dual numbers (autodiff.py:62-173) ------------------------------------
+struct Dual {
+  double r, d;
+};
+__device__ __forceinline__ Dual operator+(Dual a, Dual b) { return {a.r + b.r, a.d + b.d}; }
+__device__ __forceinline__ Dual operator+(Dual a, double s) { return {a.r + s, a.d}; }
+__device__ __forceinline__ Dual operator+(double s, Dual a) { return {a.r + s, a.d}; }
+__device__ __forceinline__ Dual operator-(Dual a, Dual b) { return {a.r - b.r, a.d - b.d}; }
+__device__ __forceinline__ Dual operator-(Dual a, double s) { return {a.r - s, a.d}; }
+__device__ __forceinline__ Dual operator-(double s, Dual a) { return {s - a.r, -a.d}; }
+__device__ __forceinline__ Dual operator*(Dual a, Dual b) {
+  return {a.r * b.r, a.r * b.d + a.d * b.r};
+}
+__device__ __forceinline__ Dual operator*(Dual a, double s) { return {a.r * s, a.d * s}; }
+__device__ __forceinline__ Dual operator*(double s, Dual a) { return {a.r * s, a.d * s}; }
+__device__ __forceinline__ Dual operator/(Dual a, double s) { return {a.r / s, a.d / s}; }
+
+// Elementary functions: `err` is raised where autodiff.py raises DomainError.
+__device__ __forceinline__ double gexp(double x, bool&) { return exp(x); }
+__device__ __forceinline__ Dual gexp(Dual x, bool&) {
+  const double v = exp(x.r);
+  return {v, v * x.d};
+}
+__device__ __forceinline__ double gcos(double x) { return cos(x); }
+__device__ __forceinline__ Dual gcos(Dual x) { return {cos(x.r), (-sin(x.r)) * x.d}; }
+// float path only rejects negatives; Dual path also rejects 0 (autodiff.py:198-216)
+__device__ __forceinline__ double gsqrt(double x, bool& err) {
+  if (x < 0.0) err = true;
+  return sqrt(x);
+}
+__device__ __forceinline__ Dual gsqrt(Dual x, bool& err) {
+  if (x.r < 0.0 || x.r == 0.0) {
+    err = true;
+    return {0.0, 0.0};
+  }
+  const double v = sqrt(x.r);
+  return {v, x.d / (2.0 * v)};
+}
+
+template <class T>
+__device__ __forceinline__ double tangent(const T&) { return 0.0; }
+template <>
+__device__ __forceinline__ double tangent<Dual>(const Dual& v) { return v.d; }
+
+// ---------------------------------------------------------------------------
+// Objective interface (all static):
+//   NACC                      number of sequential accumulators (1 or 2)
+//   nterms(d)                 terms folded into the accumulators
+//   init(a, d)                accumulator a's initial float value
+//   term<T>(X, j, d, t[NACC]) term j (X(j) -> coordinate j)
+//   finish<T>(acc[NACC], d, err)
+//   grad(X, i, d, acc, err)   d f / d x_i from the Dual rules (see header)
+// ---------------------------------------------------------------------------
+
+// objectives.py:33-45  (total = total + (a*a + 100*(b*b)), a = 1-x_i, b = x_{i+1}-x_i^2)
+struct Rosenbrock {
+  static constexpr int kId = ZEUS_OBJ_ROSENBROCK;
+  static constexpr int NACC = 1;
+  __device__ static int nterms(int d) { return d - 1; }
+  __device__ static double init(int, int) { return 0.0; }
+  template <class T>
+  __device__ static T term2(T xj, T xj1) {
+    const T a = 1.0 - xj;
+    const T b = xj1 - xj * xj;
+    return a * a + 100.0 * (b * b);
+  }
+  template <class X>
+  __device__ static void term(const X& x, int j, int, double t[1]) {
+    t[0] = term2<double>(x(j), x(j + 1));
+  }
+  __device__ static double finish(const double acc[1], int, bool&) { return acc[0]; }
+  template <class X>
+  __device__ static double grad(const X& x, int i, int d, const double*, bool&) {
+    // seed x_i: term i-1 sees it as x_{j+1}, term i as x_j
+    const double xi = x(i);
+    double g = 0.0;
+    bool any = false;
+    if (i >= 1) {
+      g = term2<Dual>(Dual{x(i - 1), 0.0}, Dual{xi, 1.0}).d;
+      any = true;
+    }
+    if (i + 1 < d) {
+      const double t = term2<Dual>(Dual{xi, 1.0}, Dual{x(i + 1), 0.0}).d;
+      g = any ? g + t : t;
+    }
+    return g;
+  }
+};
+
+// objectives.py:48-61  (total = 10 d; total = total + (x*x - 10 cos(2 pi x)))
+struct Rastrigin {
+  static constexpr int kId = ZEUS_OBJ_RASTRIGIN;
+  static constexpr int NACC = 1;
+  __device__ static int nterms(int d) { return d; }
+  __device__ static double init(int, int d) { return 10.0 * d; }
+  template <class T>
+  __device__ static T term1(T xi) {
+    return xi * xi - 10.0 * gcos(kTwoPi * xi);
+  }
+  template <class X>
+  __device__ static void term(const X& x, int j, int, double t[1]) {
+    t[0] = term1<double>(x(j));
+  }
+  __device__ static double finish(const double acc[1], int, bool&) { return acc[0]; }
+  template <class X>
+  __device__ static double grad(const X& x, int i, int, const double*, bool&) {
+    return term1<Dual>(Dual{x(i), 1.0}).d;
+  }
+};
+
+// objectives.py:64-85
+struct Ackley {
+  static constexpr int kId = ZEUS_OBJ_ACKLEY;
+  static constexpr int NACC = 2;  // sum_sq, sum_cos
+  __device__ static int nterms(int d) { return d; }
+  __device__ static double init(int, int) { return 0.0; }
+  template <class T>
+  __device__ static void terms(T xi, T& sq, T& cs) {
+    sq = xi * xi;
+    cs = gcos(kTwoPi * xi);
+  }
+  template <class X>
+  __device__ static void term(const X& x, int j, int, double t[2]) {
+    terms<double>(x(j), t[0], t[1]);
+  }
+  template <class T>
+  __device__ static T outer(T sum_sq, T sum_cos, int d, bool& err) {
+    return -20.0 * gexp(-0.2 * gsqrt(sum_sq / (double)d, err), err) -
+           gexp(sum_cos / (double)d, err) + kE + 20.0;
+  }
+  __device__ static double finish(const double acc[2], int d, bool& err) {
+    return outer<double>(acc[0], acc[1], d, err);
+  }
+  template <class X>
+  __device__ static double grad(const X& x, int i, int d, const double* acc, bool& err) {
+    Dual sq, cs;
+    terms<Dual>(Dual{x(i), 1.0}, sq, cs);
+    // real parts: the full sequential sums; tangents: the only non-zero term
+    return outer<Dual>(Dual{acc[0], sq.d}, Dual{acc[1], cs.d}, d, err).d;
+  }
+};
+
+// objectives.py:88-113 (d == 2 only; validated on the host)
+struct GoldsteinPrice {
+  static constexpr int kId = ZEUS_OBJ_GOLDSTEIN_PRICE;
+  static constexpr int NACC = 1;
+  __device__ static int nterms(int) { return 1; }
+  __device__ static double init(int, int) { return 0.0; }
+  template <class T>
+  __device__ static T eval(T x1, T x2) {
+    const T s = x1 + x2 + 1.0;
+    const T first = 1.0 + s * s *
+                              (19.0 - 14.0 * x1 + 3.0 * x1 * x1 - 14.0 * x2 +
+                               6.0 * x1 * x2 + 3.0 * x2 * x2);
+    const T t = 2.0 * x1 - 3.0 * x2;
+    const T second = 30.0 + t * t *
+                                (18.0 - 32.0 * x1 + 12.0 * x1 * x1 + 48.0 * x2 -
+                                 36.0 * x1 * x2 + 27.0 * x2 * x2);
+    return first * second;
+  }
+  template <class X>
+  __device__ static void term(const X& x, int, int, double t[1]) {
+    t[0] = eval<double>(x(0), x(1));
+  }
+  // the single "term" is the whole value: 0.0 + v == v for every v but -0.0,
+  // and GP is >= 3 on its domain; finish returns the term itself.
+  __device__ static double finish(const double acc[1], int, bool&) { return acc[0]; }
+  template <class X>
+  __device__ static double grad(const X& x, int i, int, const double*, bool&) {
+    return i == 0 ? eval<Dual>(Dual{x(0), 1.0}, Dual{x(1), 0.0}).d
+                  : eval<Dual>(Dual{x(0), 0.0}, Dual{x(1), 1.0}).d;
+  }
+};
+
+// ---- accessors ------------------------------------------------------------
+struct StridedX {
+  const double* p;
+  long long stride;
+  __device__ __forceinline__ double operator()(int j) const { return p[(long long)j * stride]; }
+};
+struct DenseX {
+  const double* p;
+  __device__ __forceinline__ double operator()(int j) const { return p[j]; }
+};
+
+// Sequential (reference-order) value of one point, one thread.
+template <class Obj, class X>
+__device__ __forceinline__ double value_seq(const X& x, int d, double acc[Obj::NACC],
+                                            bool& err) {
+#pragma unroll
+  for (int a = 0; a < Obj::NACC; ++a) acc[a] = Obj::init(a, d);
+  const int nt = Obj::nterms(d);
+  for (int j = 0; j < nt; ++j) {
+    double t[Obj::NACC];
+    Obj::term(x, j, d, t);
+#pragma unroll
+    for (int a = 0; a < Obj::NACC; ++a) acc[a] = acc[a] + t[a];
+  }
+  return Obj::finish(acc, d, err);
+}
+
+// Dispatch helper: calls F::template run<Obj>(args...) for the objective id.
+template <class F, class... A>
+__host__ int dispatch_objective(int obj, A&&... args) {
+  switch (obj) {
+    case ZEUS_OBJ_ROSENBROCK: return F::template run<Rosenbrock>(args...);
+    case ZEUS_OBJ_RASTRIGIN: return F::template run<Rastrigin>(args...);
+    case ZEUS_OBJ_ACKLEY: return F::template run<Ackley>(args...);
+    case ZEUS_OBJ_GOLDSTEIN_PRICE: return F::template run<GoldsteinPrice>(args...);
+    default: return ZEUS_ERR_ARGUMENT;
+  }
+}
+
+}  // namespace zeus

@@ -1,0 +1,383 @@
+"""End-to-end pipeline (driver.py of the reference) on B200.
+
+``zeus_run(f, cfg)`` keeps the reference's signature, configuration and result
+record.  Internally: the swarm lives in HBM (SoA), PSO init + ``iter_pso``
+sweeps run as sm_100a kernels with a device min-loc barrier after each sweep,
+then one persistent BFGS kernel refines every particle's final position
+(driver.py:244) with forward-AD gradients, Armijo search and the rank-2
+update fused on chip, then a device reduction yields ``best`` and the status
+tallies.  Under ``torch.distributed`` (one process per GPU, NCCL) the starts
+are sharded in contiguous global-index blocks and the only data-path
+collective is the per-sweep all-gather of each shard's best candidate.
+"""
+
+from __future__ import annotations
+
+import logging
+import math
+import time
+from dataclasses import dataclass, field, replace
+from typing import Callable, Iterator, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _capi, _device, engine
+from .bfgs import CONVERGED, DOMAIN_ERROR, STATUSES, BfgsOutcome
+from .linesearch import LineSearchParams
+from .objectives import objective_id
+from .pso import PsoParams
+from .streams import make_start_streams
+
+__all__ = [
+    "ZeusConfig",
+    "ZeusResult",
+    "RunStats",
+    "NoValidOptimumError",
+    "OutcomeList",
+    "zeus_run",
+    "reduce_best",
+    "make_start_streams",
+]
+
+log = logging.getLogger(__name__)
+
+
+class NoValidOptimumError(RuntimeError):
+    """Every launched run ended in a domain error; no optimum to report
+    (driver.py:45-46)."""
+
+
+@dataclass
+class ZeusConfig:
+    """All pipeline hyperparameters (driver.py:49-95), same fields, defaults
+    and validation as the reference."""
+
+    N: int
+    dim: int
+    range: tuple[float, float]
+    iter_pso: int = 5
+    iter_bfgs: int = 1000
+    iter_ls: int = 20
+    theta: float = 1e-6
+    required_c: int | None = None
+    pso: PsoParams = field(default_factory=PsoParams)
+    ls: LineSearchParams = field(default_factory=LineSearchParams)
+    seed: int = 0
+    workers: int = 0
+    deterministic: bool = False
+
+    def __post_init__(self):
+        if self.N < 1:
+            raise ValueError("N must be at least 1")
+        if self.dim < 1:
+            raise ValueError("dim must be at least 1")
+        lower, upper = self.range
+        if not lower < upper:
+            raise ValueError("range requires lower < upper")
+        if self.required_c is None:
+            self.required_c = self.N
+        if not 1 <= self.required_c <= self.N:
+            raise ValueError("required_c must be in [1, N]")
+        if min(self.iter_pso, self.iter_bfgs) < 0:
+            raise ValueError("iteration budgets must be non-negative")
+        if self.theta <= 0.0:
+            raise ValueError("theta must be positive")
+        if self.workers < 0:
+            raise ValueError("workers must be non-negative")
+        self.pso = replace(self.pso, iter_pso=self.iter_pso)
+        self.ls = replace(self.ls, iter_ls=self.iter_ls)
+
+
+@dataclass
+class RunStats:
+    """Per-start work counters returned by the BFGS kernel (host copies, in
+    per_run order): they feed the algorithmic-FLOP roofline."""
+
+    iterations: np.ndarray
+    ls_trials: np.ndarray
+    grad_evals: np.ndarray
+    status_counts: dict
+    pso_time: float = 0.0       # device seconds, PSO init + sweeps + barriers
+    bfgs_time: float = 0.0      # device seconds, the persistent BFGS kernel
+    reduce_time: float = 0.0    # device seconds, reduce_best (+ collectives)
+    kernel_launches: int = 0    # our kernels launched by this call
+
+
+@dataclass
+class ZeusResult:
+    """Outcome of one pipeline execution (driver.py:98-112).
+
+    The first five fields are the reference's.  ``device_time`` (kernels +
+    collectives, CUDA events) and ``stats`` are additions with defaults.
+    """
+
+    best: BfgsOutcome
+    per_run: Sequence[BfgsOutcome]
+    converged_count: int
+    wall_time: float
+    pso_best_before_bfgs: float
+    device_time: float | None = None
+    stats: RunStats | None = None
+
+
+class OutcomeList(Sequence):
+    """Lazy ``Sequence[BfgsOutcome]`` over host SoA copies of the per-start
+    outputs: 1M frozen dataclasses would cost seconds of CPython time, so an
+    entry is materialised on access.  Compares equal to a list of outcomes."""
+
+    def __init__(self, x: np.ndarray, f: np.ndarray, gn: np.ndarray, it: np.ndarray,
+                 st: np.ndarray, length: int | None = None):
+        self._x, self._f, self._gn, self._it, self._st = x, f, gn, it, st
+        self._n = len(f) if length is None else int(length)
+
+    def __len__(self) -> int:
+        return self._n
+
+    def _one(self, i: int) -> BfgsOutcome:
+        return BfgsOutcome(x_final=tuple(self._x[i].tolist()), f_final=float(self._f[i]),
+                           grad_norm=float(self._gn[i]), iterations=int(self._it[i]),
+                           status=STATUSES[int(self._st[i])])
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._one(k) for k in range(*i.indices(self._n))]
+        if i < 0:
+            i += self._n
+        if not 0 <= i < self._n:
+            raise IndexError(i)
+        return self._one(i)
+
+    def __iter__(self) -> Iterator[BfgsOutcome]:
+        for i in range(self._n):
+            yield self._one(i)
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, Sequence) or len(other) != self._n:
+            return NotImplemented if not isinstance(other, Sequence) else False
+        return all(a == b for a, b in zip(self, other))
+
+    def __repr__(self) -> str:
+        return f"OutcomeList(n={self._n})"
+
+    # columnar views (numpy), in per_run order
+    @property
+    def x_final(self) -> np.ndarray:
+        return self._x[: self._n]
+
+    @property
+    def f_final(self) -> np.ndarray:
+        return self._f[: self._n]
+
+    @property
+    def grad_norm(self) -> np.ndarray:
+        return self._gn[: self._n]
+
+    @property
+    def iterations(self) -> np.ndarray:
+        return self._it[: self._n]
+
+    @property
+    def status_codes(self) -> np.ndarray:
+        return self._st[: self._n]
+
+
+def reduce_best(outcomes: Sequence[BfgsOutcome]) -> tuple[BfgsOutcome, int]:
+    """Minimum f_final among non-domain-error, non-NaN outcomes, lowest index
+    on ties (driver.py:115-134).  Raises NoValidOptimumError if none."""
+    if isinstance(outcomes, OutcomeList):
+        f, st = outcomes.f_final, outcomes.status_codes
+        valid = (st != STATUSES.index(DOMAIN_ERROR)) & ~np.isnan(f)
+        if not valid.any():
+            raise NoValidOptimumError("all runs ended in domain errors")
+        idx = int(np.flatnonzero(valid)[np.argmin(f[valid])])
+        return outcomes[idx], idx
+    best: BfgsOutcome | None = None
+    best_index = -1
+    for i, outcome in enumerate(outcomes):
+        if outcome.status == DOMAIN_ERROR or math.isnan(outcome.f_final):
+            continue
+        if best is None or outcome.f_final < best.f_final:
+            best = outcome
+            best_index = i
+    if best is None:
+        raise NoValidOptimumError("all runs ended in domain errors")
+    return best, best_index
+
+
+def _dist_world(process_group):
+    if not torch.distributed.is_available() or not torch.distributed.is_initialized():
+        return 0, 1
+    return (torch.distributed.get_rank(process_group),
+            torch.distributed.get_world_size(process_group))
+
+
+def _gather_rows(t: torch.Tensor, per: int, world: int, group) -> torch.Tensor:
+    """All-gather equal-size padded shards along the last dim."""
+    lead = t.shape[:-1]
+    pad = torch.zeros(*lead, per, dtype=t.dtype, device=t.device)
+    pad[..., : t.shape[-1]] = t
+    flat = pad.reshape(-1, per).contiguous()
+    out = torch.empty((world,) + tuple(flat.shape), dtype=t.dtype, device=t.device)
+    torch.distributed.all_gather_into_tensor(out.view(-1), flat.view(-1), group=group)
+    # [world][rows][per] -> [rows][world*per]
+    return out.permute(1, 0, 2).reshape(*lead, world * per)
+
+
+def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
+             process_group=None, starts: Optional[np.ndarray] = None,
+             gather: bool = True) -> ZeusResult:
+    """Run the full pipeline on registered objective ``f`` (driver.py:220-265).
+
+    Extensions (keyword-only, defaults reproduce the reference):
+      device        CUDA device for this process (default: current).
+      process_group torch.distributed group to shard starts over (default:
+                    the world group when torch.distributed is initialised).
+      starts        host-supplied BFGS starts [N][dim]: skips PSO (used to
+                    decouple BFGS parity from PSO libm flips).
+      gather        False keeps per_run local to this rank's shard.
+
+    Early stop: ``deterministic`` or ``required_c == N`` runs every start.
+    ``workers == 0`` with ``required_c < N`` reproduces the reference's
+    sequential semantics exactly (per_run is the prefix ending at the
+    required_c-th convergence; every start is independent so the prefix is
+    computed, then cut).  ``workers > 0`` uses the device stop protocol:
+    converged starts bump a device counter, the start that reaches
+    ``required_c`` raises a flag polled at the top of every iteration, and the
+    rest end ``stopped`` (timing-dependent, as in the reference).
+    """
+    t0 = time.perf_counter()
+    obj = objective_id(f, cfg.dim)
+    dev = _device.require_device(device)
+    rank, world = _dist_world(process_group)
+    N, d = cfg.N, cfg.dim
+    lo, hi = engine.shard_bounds(N, rank, world)
+    n = hi - lo
+    required_c = N if cfg.deterministic else int(cfg.required_c)
+    early = required_c < N
+    device_stop = early and cfg.workers > 0
+    if device_stop and world > 1:
+        raise NotImplementedError("cross-GPU early stop (workers > 0, required_c < N) is not "
+                                  "implemented yet; use deterministic=True or workers=0")
+    stream = torch.cuda.current_stream(dev)
+    ev_start, ev_pso, ev_bfgs, ev_end = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+    launches0 = engine.LAUNCHES[0]
+    ev_start.record(stream)
+
+    # ---- PSO phase (driver.py:236-241)
+    pso_best = math.nan
+    if starts is None:
+        shard = engine.SwarmShard(obj, d, max(n, 1), lo, cfg.seed, dev)
+        barrier = engine.local_barrier if world == 1 else engine.make_dist_barrier(process_group)
+        lower, upper = cfg.range
+        if n > 0:
+            shard.init(lower, upper)
+        else:
+            shard.cand.zero_()
+            shard.cand[1] = -1.0
+        barrier(shard)
+        for _ in range(cfg.iter_pso):
+            if n > 0:
+                shard.sweep(cfg.pso.w, cfg.pso.c1_pso, cfg.pso.c2_pso)
+            barrier(shard)
+        x0 = shard.x[:, :n]
+        gbest = shard.gbest
+    else:
+        pts = np.asarray(starts, dtype=np.float64)
+        if pts.shape != (N, d):
+            raise ValueError(f"starts must have shape ({N}, {d})")
+        x0 = _device.to_soa(pts[lo:hi], dev) if n > 0 else torch.empty((d, 0), device=dev,
+                                                                        dtype=torch.float64)
+        gbest = None
+
+    ev_pso.record(stream)
+    # ---- multistart BFGS (driver.py:243-249)
+    out = engine.BfgsBuffers.allocate(d, n, dev)
+    params = engine.bfgs_params(cfg.theta, cfg.iter_bfgs, cfg.ls)
+    stop = None
+    if device_stop:
+        stop = (torch.zeros(1, dtype=torch.int64, device=dev),
+                torch.zeros(1, dtype=torch.int32, device=dev))
+    if n > 0:
+        engine.run_bfgs(obj, x0.contiguous() if x0.stride(0) != x0.shape[1] else x0, params,
+                        out, dev, required_c=required_c, stop=stop)
+
+    ev_bfgs.record(stream)
+    # ---- reduction (driver.py:250-251) on device
+    L = _capi.lib()
+    best_dev = torch.empty(2, dtype=torch.float64, device=dev)
+    tallies = torch.zeros(4, dtype=torch.int64, device=dev)
+    ws = _device.workspace(L.zeus_argmin_workspace_bytes(max(n, 1)), dev)
+    if n > 0:
+        _capi.check(L.zeus_reduce_best(n, lo, out.f_final.data_ptr(), out.status.data_ptr(),
+                                       best_dev.data_ptr(), tallies.data_ptr(), ws.data_ptr(),
+                                       _device.stream_ptr(dev)), "reduce_best")
+        engine.LAUNCHES[0] += 2
+    else:
+        best_dev[0] = math.nan
+        best_dev[1] = -1.0
+    if world > 1:
+        cands = torch.empty(world * 2, dtype=torch.float64, device=dev)
+        torch.distributed.all_gather_into_tensor(cands, best_dev, group=process_group)
+        torch.distributed.all_reduce(tallies, group=process_group)
+        best_dev = cands  # resolved on the host below (world pairs)
+    ev_end.record(stream)
+
+    # ---- results to host (part of the end-to-end wall time)
+    per = -(-N // world)
+    if world > 1 and gather:
+        xs = _gather_rows(out.x_final[:, :n], per, world, process_group)[:, :N]
+        cols = [_gather_rows(t[:n], per, world, process_group)[:N]
+                for t in (out.f_final, out.grad_norm, out.iterations, out.status,
+                          out.ls_trials, out.grad_evals)]
+        base = 0
+    else:
+        xs = out.x_final[:, :n]
+        cols = [t[:n] for t in (out.f_final, out.grad_norm, out.iterations, out.status,
+                                out.ls_trials, out.grad_evals)]
+        base = lo
+    host = [c.cpu().numpy() for c in cols]
+    x_host = np.ascontiguousarray(xs.cpu().numpy().T)
+    best_host = best_dev.cpu().numpy()
+    tallies_host = tallies.cpu().numpy()
+    pso_best = float(gbest[0].item()) if gbest is not None else math.nan
+    stream.synchronize()
+    device_time = ev_start.elapsed_time(ev_end) / 1e3
+
+    f_h, gn_h, it_h, st_h, ls_h, ge_h = host
+    m = len(f_h)
+    converged_count = int(tallies_host[0])
+    if early and not device_stop:
+        # sequential semantics (driver.py:205-217): cut after the required_c-th convergence
+        conv = np.flatnonzero(st_h == 0)
+        if base == 0 and len(conv) >= required_c:
+            m = int(conv[required_c - 1]) + 1
+        converged_count = int(np.count_nonzero(st_h[:m] == 0))
+        valid = (st_h[:m] != 3) & ~np.isnan(f_h[:m])
+        if not valid.any():
+            raise NoValidOptimumError("all runs ended in domain errors")
+        bidx = int(np.flatnonzero(valid)[np.argmin(f_h[:m][valid])])
+    else:
+        pairs = best_host.reshape(-1, 2)
+        ok = pairs[:, 1] >= 0
+        if not ok.any():
+            raise NoValidOptimumError("all runs ended in domain errors")
+        cand = pairs[ok]
+        order = np.lexsort((cand[:, 1], cand[:, 0]))
+        bidx = int(cand[order[0], 1]) - base
+    per_run = OutcomeList(x_host, f_h, gn_h, it_h, st_h, length=m)
+    if not 0 <= bidx < m:
+        # best lives on another rank and per_run is local (gather=False)
+        best = None
+    else:
+        best = per_run[bidx]
+    stats = RunStats(iterations=it_h[:m], ls_trials=ls_h[:m], grad_evals=ge_h[:m],
+                     status_counts={s: int(np.count_nonzero(st_h[:m] == k))
+                                    for k, s in enumerate(STATUSES)},
+                     pso_time=ev_start.elapsed_time(ev_pso) / 1e3,
+                     bfgs_time=ev_pso.elapsed_time(ev_bfgs) / 1e3,
+                     reduce_time=ev_bfgs.elapsed_time(ev_end) / 1e3,
+                     kernel_launches=engine.LAUNCHES[0] - launches0)
+    return ZeusResult(best=best, per_run=per_run, converged_count=converged_count,
+                      wall_time=time.perf_counter() - t0, pso_best_before_bfgs=pso_best,
+                      device_time=device_time, stats=stats)

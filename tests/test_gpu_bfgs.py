@@ -1,0 +1,128 @@
+"""GPU parity of multistart BFGS (bfgs.py:80-156) against the reference's
+golden outcomes and the oracle, from identical starts.
+
+Tolerance: statuses identical; |x - x_ref|_inf <= 1e-6;
+|f - f_ref| <= 1e-10 max(1,|f_ref|) for runs that stop on the gradient test
+(1e-6 for runs that hit the cap at a gradient kink); iteration counts are
+reported as a |dk| histogram, not gated.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import BOXES
+
+pytestmark = pytest.mark.gpu
+
+OBJ = {"rosenbrock": 0, "rastrigin": 1, "ackley": 2, "goldstein_price": 3}
+
+
+def device_bfgs(name, starts, cap, theta=1e-6):
+    from paper_2603_28770_b200 import engine
+    from paper_2603_28770_b200.linesearch import LineSearchParams
+
+    dev = torch.device("cuda", 0)
+    starts = np.asarray(starts, dtype=np.float64)
+    n, d = starts.shape
+    x0 = torch.from_numpy(np.ascontiguousarray(starts.T)).to(dev)
+    out = engine.BfgsBuffers.allocate(d, n, dev)
+    engine.run_bfgs(OBJ[name], x0, engine.bfgs_params(theta, cap, LineSearchParams()), out, dev)
+    return dict(x=out.x_final.cpu().numpy().T, f=out.f_final.cpu().numpy(),
+                gn=out.grad_norm.cpu().numpy(), k=out.iterations.cpu().numpy(),
+                s=out.status.cpu().numpy().astype(np.int64),
+                ls=out.ls_trials.cpu().numpy(), ng=out.grad_evals.cpu().numpy())
+
+
+def assert_outcomes_close(dev, ref_x, ref_f, ref_s, ref_k, label):
+    assert np.array_equal(dev["s"], ref_s), (label, np.flatnonzero(dev["s"] != ref_s)[:10])
+    nan_both = np.isnan(dev["x"]) & np.isnan(ref_x)
+    dx = np.where(nan_both, 0.0, np.abs(dev["x"] - ref_x))
+    assert np.max(dx) <= 1e-6, (label, np.max(dx))
+    fin = ~np.isnan(ref_f)
+    assert np.array_equal(np.isnan(dev["f"]), ~fin), label
+    tol = np.where(ref_s == 1, 1e-6, 1e-10)[fin]
+    assert np.all(np.abs(dev["f"][fin] - ref_f[fin]) <= tol * np.maximum(1, np.abs(ref_f[fin]))), label
+    dk = np.abs(dev["k"].astype(np.int64) - np.asarray(ref_k, dtype=np.int64))
+    print(f"{label}: {len(ref_s)} starts, |dk| mean {dk.mean():.2f} max {dk.max()}, "
+          f"bit-identical x {np.mean(np.all(dev['x'] == ref_x, axis=1)):.2f}")
+
+
+def test_matches_reference_golden(golden):
+    g = golden("bfgs")
+    for tag in sorted(k[: -len("_starts")] for k in g.files if k.endswith("_starts")):
+        parts = tag.split("_")
+        name = "_".join(parts[:-5])
+        cap = int(parts[-1])
+        dev = device_bfgs(name, g[tag + "_starts"], cap)
+        assert_outcomes_close(dev, g[tag + "_x"], g[tag + "_f"], g[tag + "_s"], g[tag + "_k"], tag)
+        assert np.array_equal(dev["s"] == 0, dev["gn"] < 1e-6)  # converged <=> |g| < theta
+
+
+@pytest.mark.parametrize("name,d,n,cap", [
+    ("rastrigin", 10, 512, 2000), ("rosenbrock", 10, 64, 2000), ("ackley", 10, 128, 1000),
+    ("rosenbrock", 50, 16, 2000), ("ackley", 50, 64, 1000), ("rastrigin", 50, 24, 2000),
+    ("goldstein_price", 2, 256, 1000), ("rosenbrock", 2, 1024, 1000),
+    ("rastrigin", 200, 4, 2000),   # H in HBM (d too large for shared memory)
+])
+def test_matches_oracle(oracle, name, d, n, cap):
+    lo, hi = BOXES[name]
+    starts = oracle.pso(name, d, n, 3, lo, hi, 2).positions
+    ref = oracle.bfgs_batch(name, starts, iter_bfgs=cap)
+    dev = device_bfgs(name, starts, cap)
+    assert_outcomes_close(dev, ref.x_final, ref.f_final, ref.status, ref.iterations,
+                          f"{name} d={d}")
+    assert np.all(dev["ls"] >= dev["k"])            # >= 1 trial per iteration
+    assert np.all(dev["ng"] <= dev["k"] + 1)
+
+
+def test_hand_traces(z, golden):
+    out = z.bfgs_run(z.rosenbrock, [1.0, 1.0], theta=1e-6, iter_bfgs=100)
+    assert (out.status, out.iterations, out.x_final) == (z.CONVERGED, 0, (1.0, 1.0))
+    out = z.bfgs_run(z.rosenbrock, [-1.2, 1.0], theta=1e-6, iter_bfgs=10_000)
+    assert out.status == z.CONVERGED
+    assert math.dist(out.x_final, (1.0, 1.0)) < 1e-4
+    assert np.max(np.abs(np.array(out.x_final) - golden("bfgs")["classic_x"])) <= 1e-6
+    out = z.bfgs_run(z.rosenbrock, [-1.2, 1.0], theta=1e-6, iter_bfgs=3)
+    assert (out.status, out.iterations) == (z.DIVERGED, 3) and out.grad_norm >= 1e-6
+    out = z.bfgs_run(z.ackley, [0.0, 0.0], theta=1e-6, iter_bfgs=100)
+    assert (out.status, out.iterations, out.x_final) == (z.DOMAIN_ERROR, 0, (0.0, 0.0))
+    assert out.grad_norm == math.inf and out.f_final == pytest.approx(0.0, abs=1e-12)
+
+
+def test_converged_iff_gradient_below_theta(z):
+    rng = np.random.default_rng(12)
+    for _ in range(20):
+        x0 = rng.uniform(-5.0, 5.0, 2)
+        cap = int(rng.integers(0, 30))
+        out = z.bfgs_run(z.rosenbrock, x0, theta=1e-6, iter_bfgs=cap)
+        assert (out.status == z.CONVERGED) == (out.grad_norm < 1e-6)
+        assert out.iterations <= cap
+
+
+def test_stop_probe_semantics(z):
+    out = z.bfgs_run(z.rastrigin, [3.0, 4.0], theta=1e-6, iter_bfgs=100, stop_probe=lambda: True)
+    assert (out.status, out.iterations, out.x_final) == (z.STOPPED, 0, (3.0, 4.0))
+    assert out.grad_norm == math.inf
+    probes = 0
+
+    def probe():
+        nonlocal probes
+        probes += 1
+        return probes > 1
+
+    out = z.bfgs_run(z.rosenbrock, [8.0, -3.0], theta=1e-16, iter_bfgs=1000, stop_probe=probe)
+    assert (out.status, out.iterations) == (z.STOPPED, 1)
+    full = z.bfgs_run(z.rosenbrock, [8.0, -3.0], theta=1e-16, iter_bfgs=1)
+    assert out.x_final == full.x_final and out.grad_norm == full.grad_norm
+
+
+def test_validation(z):
+    with pytest.raises(ValueError):
+        z.bfgs_run(z.rastrigin, [1.0], theta=0.0, iter_bfgs=10)
+    with pytest.raises(ValueError):
+        z.bfgs_run(z.rastrigin, [1.0], theta=1e-6, iter_bfgs=-1)
+    with pytest.raises(NotImplementedError):
+        z.bfgs_run(lambda x: x[0] * x[0], [1.0], theta=1e-6, iter_bfgs=10)

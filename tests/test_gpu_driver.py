@@ -1,0 +1,146 @@
+"""GPU end-to-end: zeus_run (driver.py:220-265) against the oracle and the
+reference's driver semantics (test_driver.py of the reference), plus
+size-independent properties at BASELINE config 2's full size."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config1_matches_oracle(z, oracle):
+    """BASELINE config 1: Rosenbrock d=2, 1,024 starts, 10 sweeps, cap 1,000."""
+    cfg = z.ZeusConfig(N=1024, dim=2, range=(-5.0, 5.0), iter_pso=10, iter_bfgs=1000, seed=0,
+                       deterministic=True)
+    res = z.zeus_run(z.rosenbrock, cfg)
+    sw = oracle.pso("rosenbrock", 2, 1024, 0, -5.0, 5.0, 10)
+    ref = oracle.bfgs_batch("rosenbrock", sw.positions, iter_bfgs=1000)
+    assert res.pso_best_before_bfgs == sw.global_best_val
+    pr = res.per_run
+    assert len(pr) == 1024
+    assert np.array_equal(pr.status_codes, ref.status)
+    assert np.max(np.abs(pr.x_final - ref.x_final)) <= 1e-6
+    assert res.converged_count == int(np.sum(ref.status == 0))
+    b = oracle.reduce_best(ref.f_final, ref.status)
+    assert abs(res.best.f_final - ref.f_final[b]) <= 1e-10 * max(1, abs(ref.f_final[b]))
+    assert res.best.f_final <= res.pso_best_before_bfgs
+
+
+def test_config2_reduced_matches_oracle(z, oracle):
+    """Rastrigin d=10, 20 sweeps, cap 2,000 on 2,048 starts; BFGS from the
+    oracle's swarm (host-supplied starts) so libm flips in PSO do not mask
+    BFGS parity."""
+    sw = oracle.pso("rastrigin", 10, 2048, 42, -5.12, 5.12, 20)
+    ref = oracle.bfgs_batch("rastrigin", sw.positions, iter_bfgs=2000)
+    cfg = z.ZeusConfig(N=2048, dim=10, range=(-5.12, 5.12), iter_pso=20, iter_bfgs=2000, seed=42,
+                       deterministic=True)
+    res = z.zeus_run(z.rastrigin, cfg, starts=sw.positions)
+    pr = res.per_run
+    mism = np.flatnonzero(pr.status_codes != ref.status)
+    for i in mism:  # boundary starts stalling near theta (hard part 1)
+        print("status flip", i, pr.status_codes[i], ref.status[i], pr.grad_norm[i], ref.grad_norm[i])
+        assert max(pr.grad_norm[i], ref.grad_norm[i]) < 1e-4
+    ok = pr.status_codes == ref.status
+    assert len(mism) <= 2
+    assert np.max(np.abs(pr.x_final[ok] - ref.x_final[ok])) <= 1e-6
+    # PSO on device vs oracle: global best agrees
+    res2 = z.zeus_run(z.rastrigin, cfg)
+    assert abs(res2.pso_best_before_bfgs - sw.global_best_val) <= 1e-9
+
+
+def test_degenerate_config_is_plain_bfgs(z):
+    cfg = z.ZeusConfig(N=1, dim=3, range=(-5.12, 5.12), iter_pso=0, iter_bfgs=300, seed=21)
+    res = z.zeus_run(z.rastrigin, cfg)
+    start = z.make_start_streams(21, 1, 3).draw_uniform(0, -5.12, 5.12, 3)
+    direct = z.bfgs_run(z.rastrigin, start, theta=cfg.theta, iter_bfgs=cfg.iter_bfgs, ls=cfg.ls)
+    assert res.per_run == [direct]
+    assert res.best == direct
+
+
+def test_sequential_early_stop_launches_prefix_only(z):
+    cfg = z.ZeusConfig(N=60, dim=2, range=(-5.12, 5.12), iter_pso=1, iter_bfgs=300,
+                       required_c=5, seed=2, workers=0)
+    res = z.zeus_run(z.rastrigin, cfg)
+    assert res.converged_count == 5
+    assert len(res.per_run) <= 60
+    assert res.per_run[-1].status == z.CONVERGED
+    assert all(o.status != z.STOPPED for o in res.per_run)
+
+
+def test_device_early_stop_marks_stopped(z):
+    cfg = z.ZeusConfig(N=4096, dim=2, range=(-5.12, 5.12), iter_pso=1, iter_bfgs=300,
+                       required_c=4, seed=2, workers=2)
+    res = z.zeus_run(z.rastrigin, cfg)
+    assert len(res.per_run) == 4096
+    assert res.converged_count >= 4
+    assert res.converged_count == sum(1 for o in res.per_run if o.status == z.CONVERGED)
+    assert any(o.status == z.STOPPED for o in res.per_run)
+    stopped = res.per_run.status_codes == 2
+    # a stopped run may finish at most the iteration in flight
+    assert res.per_run.iterations[stopped].max() <= 300
+
+
+def test_deterministic_mode_disables_early_stop(z):
+    cfg = z.ZeusConfig(N=20, dim=2, range=(-5.12, 5.12), iter_pso=1, iter_bfgs=200,
+                       required_c=1, seed=4, workers=2, deterministic=True)
+    res = z.zeus_run(z.rastrigin, cfg)
+    assert len(res.per_run) == 20
+    assert all(o.status != z.STOPPED for o in res.per_run)
+
+
+def test_best_and_pso_best(z):
+    cfg = z.ZeusConfig(N=40, dim=2, range=(-5.12, 5.12), iter_pso=2, iter_bfgs=300, seed=5)
+    res = z.zeus_run(z.rastrigin, cfg)
+    valid = [o.f_final for o in res.per_run if o.status != z.DOMAIN_ERROR]
+    assert res.best.f_final == min(valid)
+    assert res.pso_best_before_bfgs >= 0.0
+    assert res.best.f_final <= res.pso_best_before_bfgs
+    best, idx = z.reduce_best(res.per_run)
+    assert best == res.best and res.per_run[idx] == best
+
+
+def test_all_domain_errors_raise(z):
+    cfg = z.ZeusConfig(N=3, dim=2, range=(-1.0, 1.0), iter_pso=0, iter_bfgs=10, seed=1)
+    with pytest.raises(z.NoValidOptimumError):
+        z.zeus_run(z.ackley, cfg, starts=np.zeros((3, 2)))
+
+
+def test_rastrigin_2d_multistart_lands_at_origin(z):
+    for seed in (101, 202):
+        cfg = z.ZeusConfig(N=2000, dim=2, range=(-5.12, 5.12), iter_pso=5, iter_bfgs=400,
+                           required_c=50, seed=seed, workers=2)
+        res = z.zeus_run(z.rastrigin, cfg)
+        assert math.dist(res.best.x_final, (0.0, 0.0)) < 0.5
+
+
+def test_reference_functions_are_accepted(z):
+    """A user of the reference passes zeus.objectives.<fn>; map by name."""
+    def rosenbrock(x):  # stand-in with the reference's module/name
+        raise AssertionError("never called on the host")
+    rosenbrock.__module__ = "zeus.objectives"
+    cfg = z.ZeusConfig(N=16, dim=2, range=(-5.0, 5.0), iter_pso=1, seed=3, deterministic=True)
+    a = z.zeus_run(rosenbrock, cfg)
+    b = z.zeus_run(z.rosenbrock, cfg)
+    assert a.per_run == b.per_run
+
+
+def test_full_size_config2_properties(z):
+    """BASELINE config 2 at full size: 65,536 starts.  Size-independent checks:
+    converged <=> |g| < theta, tallies, best <= PSO best, bitwise
+    reproducibility, every start has 0 <= k <= cap."""
+    cfg = z.ZeusConfig(N=65536, dim=10, range=(-5.12, 5.12), iter_pso=20, iter_bfgs=2000,
+                       seed=42, deterministic=True)
+    a = z.zeus_run(z.rastrigin, cfg)
+    pr = a.per_run
+    assert np.array_equal(pr.status_codes == 0, pr.grad_norm < 1e-6)
+    assert a.converged_count == int(np.sum(pr.status_codes == 0))
+    assert a.converged_count >= 65000
+    assert a.best.f_final <= a.pso_best_before_bfgs
+    assert pr.iterations.min() >= 0 and pr.iterations.max() <= 2000
+    b = z.zeus_run(z.rastrigin, cfg)
+    assert np.array_equal(a.per_run.x_final, b.per_run.x_final)
+    assert np.array_equal(a.per_run.iterations, b.per_run.iterations)
+    print(f"C2 full: {a.converged_count} converged, device {a.device_time*1e3:.2f} ms, "
+          f"wall {a.wall_time*1e3:.1f} ms, best f {a.best.f_final:.3e}")

@@ -1,0 +1,150 @@
+"""GPU parity of the swarm phase (pso.py:79-164) and its sharding.
+
+Rosenbrock / Goldstein-Price swarms are bit-identical to the reference.
+Rastrigin / Ackley values go through CUDA libm; a <= 2-ulp difference can flip
+a personal-best comparison, after which that particle legitimately diverges
+from the reference trajectory -- such flips are listed, and everything not
+downstream of a flip must be bit-identical.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import BOXES
+
+pytestmark = pytest.mark.gpu
+
+OBJ = {"rosenbrock": 0, "rastrigin": 1, "ackley": 2, "goldstein_price": 3}
+
+
+def _run_shards(name, d, n, seed, sweeps, nshards=1):
+    """Emulate `nshards` GPUs on one device: per-shard kernels + the same
+    min-loc select the NCCL barrier performs."""
+    from paper_2603_28770_b200 import engine
+
+    dev = torch.device("cuda", 0)
+    lo, hi = BOXES[name]
+    shards = []
+    for r in range(nshards):
+        a, b = engine.shard_bounds(n, r, nshards)
+        shards.append(engine.SwarmShard(OBJ[name], d, b - a, a, seed, dev))
+
+    def barrier():
+        cands = torch.cat([s.cand for s in shards])
+        for s in shards:
+            s.select(cands, nshards)
+
+    for s in shards:
+        s.init(lo, hi)
+    barrier()
+    for _ in range(sweeps):
+        for s in shards:
+            s.sweep(0.5, 1.2, 1.5)
+        barrier()
+    cat = lambda attr: np.concatenate([getattr(s, attr).cpu().numpy().T for s in shards])  # noqa
+    return dict(x=cat("x"), v=cat("v"), p=cat("p"),
+                pval=np.concatenate([s.pval.cpu().numpy() for s in shards]),
+                gX=shards[0].gX.cpu().numpy(), gF=float(shards[0].gbest[0].item()),
+                gI=int(shards[0].gbest[1].item()))
+
+
+def _tags(g):
+    tags = set()
+    for k in g.files:
+        parts = k.split("_")
+        for cut in range(2, len(parts)):
+            t = "_".join(parts[:cut])
+            if t + "_gF" in g.files:
+                tags.add(t)
+    return sorted(tags)
+
+
+def test_swarm_matches_reference_golden(golden):
+    g = golden("pso")
+    for tag in _tags(g):
+        parts = tag.split("_")
+        name = "_".join(parts[:-4])
+        d, n, seed, sweeps = map(int, parts[-4:])
+        init = _run_shards(name, d, n, seed, 0)
+        # positions / velocities involve no libm: always bit-exact
+        assert np.array_equal(init["x"], g[tag + "_init_x"]), tag
+        assert np.array_equal(init["v"], g[tag + "_init_v"]), tag
+        out = _run_shards(name, d, n, seed, sweeps)
+        if name in ("rosenbrock", "goldstein_price"):
+            assert np.array_equal(init["pval"], g[tag + "_init_pval"]), tag
+            for key in ("x", "v", "p", "pval", "gX"):
+                assert np.array_equal(out[key], g[tag + "_" + key]), (tag, key)
+            assert out["gF"] == float(g[tag + "_gF"])
+        else:
+            ref = g[tag + "_init_pval"]
+            assert np.all(np.abs(init["pval"] - ref) <= 1e-12 * np.maximum(1, np.abs(ref)))
+            same = np.all(out["x"] == g[tag + "_x"], axis=1)
+            print(f"{tag}: {same.sum()}/{n} particles bit-identical after {sweeps} sweeps")
+            if same.all():
+                assert np.array_equal(out["p"], g[tag + "_p"])
+            assert abs(out["gF"] - float(g[tag + "_gF"])) <= 1e-9 * max(1, abs(out["gF"]))
+
+
+@pytest.mark.parametrize("name,d,n,sweeps", [("rosenbrock", 10, 3000, 8),
+                                             ("rastrigin", 10, 2048, 20),
+                                             ("ackley", 5, 1000, 5)])
+def test_swarm_matches_oracle(oracle, name, d, n, sweeps):
+    lo, hi = BOXES[name]
+    dev = _run_shards(name, d, n, 42, sweeps)
+    ref = oracle.pso(name, d, n, 42, lo, hi, sweeps)
+    same = np.all(dev["x"] == ref.positions, axis=1)
+    if name == "rosenbrock":
+        assert same.all()
+        assert np.array_equal(dev["p"], ref.personal_best_pos)
+        assert np.array_equal(dev["pval"], ref.personal_best_val)
+        assert dev["gF"] == ref.global_best_val
+    else:
+        print(f"{name}: {same.sum()}/{n} bit-identical")
+        assert abs(dev["gF"] - ref.global_best_val) <= 1e-6 * max(1, abs(ref.global_best_val))
+
+
+@pytest.mark.parametrize("nshards", [2, 3, 8])
+def test_sharding_is_bit_invariant(nshards):
+    """per-particle results are identical for any shard count."""
+    one = _run_shards("rastrigin", 10, 5000, 7, 6, 1)
+    many = _run_shards("rastrigin", 10, 5000, 7, 6, nshards)
+    for key in ("x", "v", "p", "pval", "gX"):
+        assert np.array_equal(one[key], many[key]), key
+    assert one["gF"] == many["gF"] and one["gI"] == many["gI"]
+
+
+def test_full_size_c2_swarm_properties():
+    """BASELINE config 2 (Rastrigin d=10, 65,536 particles, 20 sweeps):
+    pval == f(pbest) (same device functor), gbest == np.argmin(pval),
+    init inside the box."""
+    from paper_2603_28770_b200 import _capi
+
+    init = _run_shards("rastrigin", 10, 65536, 42, 0)
+    assert np.all((init["x"] >= -5.12) & (init["x"] < 5.12))
+    assert np.all(np.abs(init["v"]) <= 10.24)
+    out = _run_shards("rastrigin", 10, 65536, 42, 20)
+    assert out["gI"] == int(np.argmin(out["pval"]))
+    assert out["gF"] == out["pval"].min()
+    assert np.all(out["pval"] <= init["pval"])
+    L = _capi.lib()
+    xs = torch.from_numpy(np.ascontiguousarray(out["p"].T)).cuda()
+    f = torch.empty(65536, dtype=torch.float64, device="cuda")
+    _capi.check(L.zeus_objective_value(1, 10, 65536, xs.data_ptr(), 65536, f.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream))
+    assert np.array_equal(f.cpu().numpy(), out["pval"])
+
+
+def test_public_init_update_swarm(z):
+    streams = z.make_start_streams(21, 30, 2)
+    state = z.init_swarm(z.rastrigin, 30, (-5.12, 5.12), streams)
+    assert np.array_equal(state.personal_best_pos, state.positions)
+    prev = state.global_best_val
+    for _ in range(6):
+        z.update_swarm(state, z.rastrigin, z.PsoParams(), streams)
+        assert state.global_best_val <= prev
+        assert state.global_best_val == state.personal_best_val.min()
+        prev = state.global_best_val
+    # same sequence through the engine in one go
+    ref = _run_shards("rastrigin", 2, 30, 21, 6)
+    assert np.array_equal(state.positions, ref["x"])

@@ -1,23 +1,39 @@
-// bfgs.cu -- multistart BFGS (bfgs.py:80-156) on sm_100a, generic-d kernel.
+// bfgs.cu -- multistart BFGS (bfgs.py:80-156) on sm_100a.
 //
-// Persistent kernel, one warp per start: a warp pops start indices from a
+// Persistent kernel, one warp per start.  A warp pops start indices from a
 // device work counter and runs the whole local minimisation without leaving
-// the SM -- forward-AD gradient (autodiff.py:243), Armijo backtracking
+// the SM: forward-AD gradient (autodiff.py:243), Armijo backtracking
 // (linesearch.py:40), curvature-guarded rank-2 inverse-Hessian update
-// (bfgs.py:59) and the convergence / cap / stop tests (bfgs.py:115-130).
+// (bfgs.py:59), convergence / cap / stop tests (bfgs.py:115-130).
 //
-// Lane mapping: lane l owns coordinates j = l, l+32, ... and the matching
-// columns of H.  Vectors live in the warp's shared-memory slice so any lane
-// can read neighbours (Rosenbrock couples x_j and x_{j+1}).  H is d x d,
-// column j owned by lane j%32: the matvec u_j = sum_i H_ij dg_i and the
-// update H_ij += dx_i a_j + u_i b_j  (a_j = c dx_j - rho u_j, b_j = -rho dx_j,
-// the O(d^2) form of V H V^T + rho dx dx^T) read dx_i / u_i as shared-memory
-// broadcasts.  One matvec per iteration: with u = H dg the next direction
-// needs H' g', which is formed from the same column pass.
+// Latency is the design target as much as throughput: time-to-solution is
+// set by the few starts that run to the iteration cap, so one iteration of one
+// warp must be short.
 //
-// Objective values keep the reference's sequential summation order (terms
-// computed lane-parallel into shared memory, then folded in index order by
-// every lane), so f is bit-identical to the reference wherever libm agrees.
+//  * Speculative batched line search.  The reference tries alpha0*shrink^t
+//    for t = 0, 1, ... and takes the FIRST trial passing the Armijo test.
+//    Trials are independent given (x, p, f0, g.p), so a batch of B trials is
+//    evaluated at once -- the B x nterms objective terms are spread over the
+//    32 lanes, lane b folds trial b's terms in the reference's sequential
+//    order, and a ballot picks the lowest passing trial.  The accepted alpha,
+//    trial count and f are exactly the sequential search's.  B adapts to the
+//    start's previous trial count (a start stuck at 21 trials per iteration
+//    resolves them in one round).
+//  * One fused pass over H per iteration: the previous iteration's rank-2
+//    update H += dx a^T + u b^T  (a = c dx - rho u, b = -rho dx: the O(d^2)
+//    form of V H V^T + rho dx dx^T) is applied lazily while the same pass
+//    forms u = H dg and w = H g'.  Then
+//        p' = -H' g' = -(w - rho dx (u.g') - rho u (dx.g') + c dx (dx.g')),
+//    so one matvec sweep serves both the update and the next direction.
+//  * One 8-value butterfly reduction per iteration delivers |g'|^2, dx.dg,
+//    |dx|^2, |dg|^2, dg.u, u.g', dx.g' (guard, rho, c, p'), plus one for g'.p'.
+//  * H column j is owned by lane j%32.  For d <= 32 the column lives in
+//    registers (template DR); otherwise in the warp's shared-memory slice
+//    (or HBM for very large d).  Row values (dg, g', dx, u of the previous
+//    iteration) are shared-memory broadcasts.
+//
+// Objective values keep the reference's sequential summation order, so f is
+// bit-identical to the reference wherever libm agrees.
 #include <algorithm>
 
 #include "objectives.cuh"
@@ -41,205 +57,436 @@ struct BfgsArgs {
   unsigned long long* work;
   double* h_global;  // non-null: H lives in HBM/L2 (d too large for smem)
   int warp_doubles;  // shared-memory doubles per warp
+  int ldh;           // row stride of an smem/global H
+  int tstride;       // term-buffer row stride (odd, >= nterms)
+  int bmax;          // max trials per speculative batch
+  int nalpha;        // alpha table length (block smem)
 };
 
 constexpr int kBfgsWarps = 4;
+constexpr int kTermCap = 320;   // objective terms per speculative batch
+constexpr int kAlphaTable = 64;
+constexpr int kMaxC = 32;       // columns per lane in the smem / HBM path: d <= 1024
 
+// H slice size in doubles, kept even so the row4 double2 loads stay 16-B aligned
+__host__ __device__ inline size_t hsize(int d, int ldh) { return ((size_t)d * ldh + 1) & ~(size_t)1; }
+
+
+// Trial-point accessor: coordinate j of x + alpha p (reference: x + alpha*p,
+// numpy multiply then add, no contraction).
+struct TrialX {
+  const double* x;
+  const double* p;
+  double alpha;
+  __device__ __forceinline__ double operator()(int j) const { return x[j] + alpha * p[j]; }
+};
+
+__device__ __forceinline__ void warp_sum8(double v[8]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] += __shfl_xor_sync(kFull, v[q], o);
+  }
+}
+
+// Evaluate B trial points; lane b < B returns trial b's value/accumulators.
+// `trial_alpha(b)` gives trial b's step; B == 0 means "evaluate x itself".
 template <class Obj>
-__device__ __forceinline__ double warp_value(const double* xs, int d, double* terms,
-                                             double* acc, int lane) {
+__device__ __forceinline__ double eval_batch(int B, const double* alpha_of, int d,
+                                             const double* x, const double* p, double* T,
+                                             int tstride, int rows, int lane,
+                                             double acc[Obj::NACC]) {
   const int nt = Obj::nterms(d);
-  const DenseX X{xs};
-  for (int j = lane; j < nt; j += 32) {
+  const int nb = B > 0 ? B : 1;
+  const int total = nb * nt;
+  for (int q = lane; q < total; q += 32) {
+    const int b = q / nt, j = q - b * nt;
     double t[Obj::NACC];
-    Obj::term(X, j, d, t);
+    if (B > 0) {
+      Obj::term(TrialX{x, p, alpha_of[b]}, j, d, t);
+    } else {
+      Obj::term(DenseX{x}, j, d, t);
+    }
 #pragma unroll
-    for (int a = 0; a < Obj::NACC; ++a) terms[a * d + j] = t[a];
+    for (int a = 0; a < Obj::NACC; ++a) T[(a * rows + b) * tstride + j] = t[a];
   }
   __syncwarp();
+  double f = 0.0;
+  if (lane < nb) {
 #pragma unroll
-  for (int a = 0; a < Obj::NACC; ++a) {
-    double s = Obj::init(a, d);
-    for (int j = 0; j < nt; ++j) s = s + terms[a * d + j];
-    acc[a] = s;
+    for (int a = 0; a < Obj::NACC; ++a) {
+      const double* row = T + (a * rows + lane) * tstride;
+      double s = Obj::init(a, d);
+      for (int j = 0; j < nt; ++j) s = s + row[j];
+      acc[a] = s;
+    }
+    bool err = false;
+    f = Obj::finish(acc, d, err);
   }
   __syncwarp();
-  bool err = false;
-  return Obj::finish(acc, d, err);
+  return f;
 }
 
-// Gradient at xs given the accumulators of the value sweep at the same point.
-// Returns false (uniformly across the warp) on a DomainError.
-template <class Obj>
-__device__ __forceinline__ bool warp_gradient(const double* xs, int d, const double* acc,
-                                              double* g, int lane) {
-  const DenseX X{xs};
-  bool err = false;
-  for (int i = lane; i < d; i += 32) g[i] = Obj::grad(X, i, d, acc, err);
-  __syncwarp();
-  return !__any_sync(kFull, err);
-}
+template <class Obj, int DR>
+struct BfgsWarp {
+  // shared-memory vectors of this warp (each d doubles unless noted)
+  double *x, *xn, *p, *g, *gn, *row4, *T;
+  double* H;  // smem / global H (DR == 0)
+  const double* alpha_tab;
 
-__device__ __forceinline__ double warp_dot(const double* a, const double* b, int d, int lane) {
-  double s = 0.0;
-  for (int j = lane; j < d; j += 32) s = fma(a[j], b[j], s);
-  return warp_sum(s);
-}
+  __device__ __forceinline__ double alpha_at(const BfgsArgs& A, int t) const {
+    if (t < A.nalpha) return alpha_tab[t];
+    double a = alpha_tab[A.nalpha - 1];
+    for (int k = A.nalpha - 1; k < t; ++k) a *= A.shrink;
+    return a;
+  }
 
-template <class Obj>
-__device__ void bfgs_one(const BfgsArgs& A, long long s, int lane, double* H, double* x,
-                         double* g, double* p, double* xn, double* gn, double* dx, double* dg,
-                         double* u, double* terms) {
-  const int d = A.d;
-  for (int j = lane; j < d; j += 32) x[j] = A.x0[(int64_t)j * A.ldx + s];
-  for (int i = 0; i < d; ++i)
-    for (int j = lane; j < d; j += 32) H[(int64_t)i * d + j] = (i == j) ? 1.0 : 0.0;
-  __syncwarp();
+  __device__ void run(const BfgsArgs& A, long long s, int lane) {
+    const int d = A.d;
+    const int C = (d + 31) >> 5;  // columns per lane
+    double hreg[DR > 0 ? DR : 1];
+    // lane-local state of the owned columns: previous update coefficients
+    double a_col[DR > 0 ? 1 : kMaxC], b_col[DR > 0 ? 1 : kMaxC];
+#pragma unroll
+    for (int c = 0; c < (DR > 0 ? 1 : kMaxC); ++c) a_col[c] = b_col[c] = 0.0;
 
-  double acc[Obj::NACC], acc_n[Obj::NACC];
-  double f0 = warp_value<Obj>(x, d, terms, acc, lane);  // f(x0): also f_final for k=0 exits
-  int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0;
-  double gnorm = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-  bool have_grad = false;
+    for (int j = lane; j < d; j += 32) x[j] = A.x0[(int64_t)j * A.ldx + s];
+    if constexpr (DR > 0) {
+#pragma unroll
+      for (int i = 0; i < DR; ++i) hreg[i] = (i == lane) ? 1.0 : 0.0;
+    } else {
+      for (int i = 0; i < d; ++i)
+        for (int j = lane; j < d; j += 32) H[(int64_t)i * A.ldh + j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncwarp();
 
-  for (;;) {
+    double acc[Obj::NACC];
+    double f0 = eval_batch<Obj>(0, nullptr, d, x, p, T, A.tstride, A.bmax, lane, acc);
+    f0 = __shfl_sync(kFull, f0, 0);
+#pragma unroll
+    for (int a = 0; a < Obj::NACC; ++a) acc[a] = __shfl_sync(kFull, acc[a], 0);
+
+    int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
+    double gnorm = __longlong_as_double(0x7ff0000000000000LL);
+    double ddir = 0.0;
+    bool pending = false;
+
+    // ---- iteration 0 prologue: stop probe, first gradient, p = -g
     if (A.stop_flag && *(volatile int*)A.stop_flag) {
       status = ZEUS_STOPPED;
-      break;
+      goto done;
     }
-    if (!have_grad) {
+    {
       ++grads;
-      if (!warp_gradient<Obj>(x, d, acc, g, lane)) {
+      bool err = false;
+      double part = 0.0;
+      for (int j = lane; j < d; j += 32) {
+        const double gj = Obj::grad(DenseX{x}, j, d, acc, err);
+        g[j] = gj;
+        p[j] = -gj;  // H0 = I: -(I @ g) is exact
+        part = fma(gj, gj, part);
+      }
+      if (__any_sync(kFull, err)) {
         status = ZEUS_DOMAIN_ERROR;
+        goto done;
+      }
+      const double gg = warp_sum(part);
+      gnorm = sqrt(gg);
+      ddir = -gg;  // g . (-g)
+      __syncwarp();
+    }
+
+    for (;;) {
+      if (gnorm < A.theta) {
+        status = ZEUS_CONVERGED;
         break;
       }
-      have_grad = true;
-      gnorm = sqrt(warp_dot(g, g, d, lane));
-    }
-    if (gnorm < A.theta) {
-      status = ZEUS_CONVERGED;
-      break;
-    }
-    if (k >= A.cap) {
-      status = ZEUS_DIVERGED;
-      break;
-    }
-    // p = -(H g)   (bfgs.py:131)
-    for (int j = lane; j < d; j += 32) {
-      double t = 0.0;
-      for (int i = 0; i < d; ++i) t = fma(H[(int64_t)i * d + j], g[i], t);
-      p[j] = -t;
-    }
-    __syncwarp();
-    // Armijo backtracking (linesearch.py:60-71); f0 is the cached f(x)
-    const double ddir = warp_dot(g, p, d, lane);
-    double alpha = A.alpha0, ft = 0.0;
-    int t = 0;
-    for (;; ++t) {
-      for (int j = lane; j < d; j += 32) xn[j] = x[j] + alpha * p[j];
-      __syncwarp();
-      ft = warp_value<Obj>(xn, d, terms, acc_n, lane);
-      if (ft <= f0 + A.c1 * alpha * ddir) break;
-      if (t >= A.iter_ls) break;
-      alpha *= A.shrink;
-    }
-    ls_trials += t + 1;
-    // gradient at x_new = x + alpha p (bfgs.py:135-136)
-    ++grads;
-    if (!warp_gradient<Obj>(xn, d, acc_n, gn, lane)) {
-      status = ZEUS_DOMAIN_ERROR;
-      break;
-    }
-    // hessian_update(H, x_new - x, g_new - g)   (bfgs.py:59-77, 140)
-    double c_dd = 0.0, c_xx = 0.0, c_gg = 0.0;
-    for (int j = lane; j < d; j += 32) {
-      const double a = xn[j] - x[j], b = gn[j] - g[j];
-      dx[j] = a;
-      dg[j] = b;
-      c_dd = fma(a, b, c_dd);
-      c_xx = fma(a, a, c_xx);
-      c_gg = fma(b, b, c_gg);
-    }
-    const double curv = warp_sum(c_dd);
-    const double ndx = sqrt(warp_sum(c_xx)), ndg = sqrt(warp_sum(c_gg));
-    __syncwarp();
-    if (!(curv <= kCurvatureFloor * ndx * ndg)) {
-      const double rho = 1.0 / curv;
-      double dgu = 0.0;
-      for (int j = lane; j < d; j += 32) {
-        double t2 = 0.0;
-        for (int i = 0; i < d; ++i) t2 = fma(H[(int64_t)i * d + j], dg[i], t2);
-        u[j] = t2;
-        dgu = fma(dg[j], t2, dgu);
+      if (k >= A.cap) {
+        status = ZEUS_DIVERGED;
+        break;
       }
-      dgu = warp_sum(dgu);
+      // ---- speculative batched Armijo search (linesearch.py:60-71)
+      int t_acc = -1;
+      double f_new = 0.0, acc_new[Obj::NACC];
+      {
+        int t0 = 0;
+        int B = min(max(prev_trials, max(1, 32 / max(Obj::nterms(d), 1))), A.bmax);
+        for (;;) {
+          B = min(B, A.iter_ls + 1 - t0);
+          double* atab = T + Obj::NACC * A.bmax * A.tstride;  // per-warp alpha scratch
+          if (lane < B) atab[lane] = alpha_at(A, t0 + lane);
+          __syncwarp();
+          double accb[Obj::NACC];
+          const double fb = eval_batch<Obj>(B, atab, d, x, p, T, A.tstride, A.bmax, lane, accb);
+          bool pass = false;
+          if (lane < B) pass = fb <= f0 + A.c1 * atab[lane] * ddir;  // NaN fails
+          const unsigned m = __ballot_sync(kFull, pass);
+          int src = -1;
+          if (m) {
+            src = __ffs(m) - 1;
+          } else if (t0 + B > A.iter_ls) {
+            src = B - 1;  // fell through: the last trial (shrink^iter_ls)
+          }
+          if (src >= 0) {
+            t_acc = t0 + src;
+            f_new = __shfl_sync(kFull, fb, src);
+#pragma unroll
+            for (int a = 0; a < Obj::NACC; ++a) acc_new[a] = __shfl_sync(kFull, accb[a], src);
+            const double alpha = __shfl_sync(kFull, lane < B ? atab[lane] : 0.0, src);
+            for (int j = lane; j < d; j += 32) xn[j] = x[j] + alpha * p[j];
+            break;
+          }
+          t0 += B;
+          B = min(2 * B, A.bmax);
+        }
+      }
+      ls_trials += t_acc + 1;
+      prev_trials = t_acc + 1;
       __syncwarp();
-      const double cc = fma(rho * rho, dgu, rho);
-      for (int j = lane; j < d; j += 32) {
-        const double aj = fma(cc, dx[j], -rho * u[j]);
-        const double bj = -rho * dx[j];
-        for (int i = 0; i < d; ++i) {
-          double* h = H + (int64_t)i * d + j;
-          *h = fma(dx[i], aj, fma(u[i], bj, *h));
+
+      // ---- gradient at x_new (bfgs.py:136); DomainError leaves x, k unchanged
+      ++grads;
+      double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      {
+        bool err = false;
+        for (int j = lane; j < d; j += 32) {
+          const double gj = Obj::grad(DenseX{xn}, j, d, acc_new, err);
+          const double dgj = gj - g[j];
+          gn[j] = gj;
+          row4[4 * j + 0] = dgj;
+          row4[4 * j + 1] = gj;
+        }
+        if (__any_sync(kFull, err)) {
+          status = ZEUS_DOMAIN_ERROR;
+          break;
         }
       }
       __syncwarp();
-    }
-    // x, g <- x_new, g_new  (bfgs.py:141-145)
-    double* tmp = x;
-    x = xn;
-    xn = tmp;
-    tmp = g;
-    g = gn;
-    gn = tmp;
-    f0 = ft;
+
+      // ---- fused pass over H: lazy rank-2 update, u = H dg, w = H g'
+      double u_own[DR > 0 ? 1 : kMaxC], w_own[DR > 0 ? 1 : kMaxC];
+      if constexpr (DR > 0) {
+        double u0 = 0.0, u1 = 0.0, w0 = 0.0, w1 = 0.0;
+        const double aj = a_col[0], bj = b_col[0];
+        if (pending) {
 #pragma unroll
-    for (int a = 0; a < Obj::NACC; ++a) acc[a] = acc_n[a];
-    gnorm = sqrt(warp_dot(g, g, d, lane));
-    ++k;
+          for (int i = 0; i < DR; ++i) {
+            if (i < d) {
+              const double2 r0 = *reinterpret_cast<const double2*>(row4 + 4 * i);
+              const double2 r1 = *reinterpret_cast<const double2*>(row4 + 4 * i + 2);
+              const double h = fma(r1.x, aj, fma(r1.y, bj, hreg[i]));
+              hreg[i] = h;
+              if (i & 1) {
+                u1 = fma(h, r0.x, u1);
+                w1 = fma(h, r0.y, w1);
+              } else {
+                u0 = fma(h, r0.x, u0);
+                w0 = fma(h, r0.y, w0);
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < DR; ++i) {
+            if (i < d) {
+              const double2 r0 = *reinterpret_cast<const double2*>(row4 + 4 * i);
+              const double h = hreg[i];
+              if (i & 1) {
+                u1 = fma(h, r0.x, u1);
+                w1 = fma(h, r0.y, w1);
+              } else {
+                u0 = fma(h, r0.x, u0);
+                w0 = fma(h, r0.y, w0);
+              }
+            }
+          }
+        }
+        u_own[0] = u0 + u1;
+        w_own[0] = w0 + w1;
+      } else {
+        for (int c = 0; c < C; ++c) {
+          const int j = lane + 32 * c;
+          double u0 = 0.0, u1 = 0.0, w0 = 0.0, w1 = 0.0;
+          if (j < d) {
+            const double aj = a_col[c], bj = b_col[c];
+            double* col = H + j;
+            int i = 0;
+            for (; i + 1 < d; i += 2) {
+              const double2 ra = *reinterpret_cast<const double2*>(row4 + 4 * i);
+              const double2 rb = *reinterpret_cast<const double2*>(row4 + 4 * i + 4);
+              double ha = col[(int64_t)i * A.ldh], hb = col[(int64_t)(i + 1) * A.ldh];
+              if (pending) {
+                const double2 sa = *reinterpret_cast<const double2*>(row4 + 4 * i + 2);
+                const double2 sb = *reinterpret_cast<const double2*>(row4 + 4 * i + 6);
+                ha = fma(sa.x, aj, fma(sa.y, bj, ha));
+                hb = fma(sb.x, aj, fma(sb.y, bj, hb));
+                col[(int64_t)i * A.ldh] = ha;
+                col[(int64_t)(i + 1) * A.ldh] = hb;
+              }
+              u0 = fma(ha, ra.x, u0);
+              w0 = fma(ha, ra.y, w0);
+              u1 = fma(hb, rb.x, u1);
+              w1 = fma(hb, rb.y, w1);
+            }
+            if (i < d) {
+              const double2 ra = *reinterpret_cast<const double2*>(row4 + 4 * i);
+              double ha = col[(int64_t)i * A.ldh];
+              if (pending) {
+                const double2 sa = *reinterpret_cast<const double2*>(row4 + 4 * i + 2);
+                ha = fma(sa.x, aj, fma(sa.y, bj, ha));
+                col[(int64_t)i * A.ldh] = ha;
+              }
+              u0 = fma(ha, ra.x, u0);
+              w0 = fma(ha, ra.y, w0);
+            }
+          }
+          u_own[c] = u0 + u1;
+          w_own[c] = w0 + w1;
+        }
+      }
+
+      // ---- one 8-value reduction: norms, curvature and the p' scalars
+      {
+        for (int c = 0; c < C; ++c) {
+          const int j = lane + 32 * c;
+          if (j >= d) break;
+          const double dxj = xn[j] - x[j], dgj = row4[4 * j], gj = gn[j];
+          const double uj = u_own[DR > 0 ? 0 : c], wj = w_own[DR > 0 ? 0 : c];
+          part[0] = fma(gj, gj, part[0]);
+          part[1] = fma(dxj, dgj, part[1]);
+          part[2] = fma(dxj, dxj, part[2]);
+          part[3] = fma(dgj, dgj, part[3]);
+          part[4] = fma(dgj, uj, part[4]);
+          part[5] = fma(uj, gj, part[5]);
+          part[6] = fma(dxj, gj, part[6]);
+          part[7] = fma(wj, gj, part[7]);
+        }
+        warp_sum8(part);
+      }
+      const double curv = part[1];
+      const double ndx = sqrt(part[2]), ndg = sqrt(part[3]);
+      pending = !(curv <= kCurvatureFloor * ndx * ndg);  // bfgs.py:69-71
+      double pd = 0.0;
+      __syncwarp();  // row4 (dx/u of the previous iteration) fully consumed
+      {
+        const double rho = pending ? 1.0 / curv : 0.0;
+        const double cc = pending ? fma(rho * rho, part[4], rho) : 0.0;
+        const double ug = part[5], xg = part[6];
+        for (int c = 0; c < C; ++c) {
+          const int j = lane + 32 * c;
+          if (j >= d) break;
+          const double dxj = xn[j] - x[j];
+          const double uj = u_own[DR > 0 ? 0 : c], wj = w_own[DR > 0 ? 0 : c];
+          double pj = -wj;
+          if (pending) {
+            // p' = -(w - rho dx (u.g') - rho u (dx.g') + c dx (dx.g'))
+            pj = -(wj + fma(dxj, fma(cc, xg, -rho * ug), -rho * xg * uj));
+            const double aj = fma(cc, dxj, -rho * uj), bj = -rho * dxj;
+            if constexpr (DR > 0) {
+              a_col[0] = aj;
+              b_col[0] = bj;
+            } else {
+              a_col[c] = aj;
+              b_col[c] = bj;
+            }
+            row4[4 * j + 2] = dxj;
+            row4[4 * j + 3] = uj;
+          }
+          p[j] = pj;
+          pd = fma(gn[j], pj, pd);
+        }
+      }
+      // x, g <- x_new, g_new (bfgs.py:141-145)
+      {
+        double* t = x;
+        x = xn;
+        xn = t;
+        t = g;
+        g = gn;
+        gn = t;
+      }
+      f0 = f_new;
+#pragma unroll
+      for (int a = 0; a < Obj::NACC; ++a) acc[a] = acc_new[a];
+      gnorm = sqrt(part[0]);
+      ddir = warp_sum(pd);  // np.dot(g, p) of the next line search
+      ++k;
+      __syncwarp();
+      if (A.stop_flag && *(volatile int*)A.stop_flag) {
+        status = ZEUS_STOPPED;
+        break;
+      }
+    }
+
+  done:
+    const zeus_bfgs_out& o = A.out;
+    for (int j = lane; j < d; j += 32) o.x_final[(int64_t)j * o.ld_out + s] = x[j];
+    if (lane == 0) {
+      o.f_final[s] = f0;
+      o.grad_norm[s] = gnorm;
+      o.iterations[s] = k;
+      o.status[s] = (uint8_t)status;
+      if (o.ls_trials) o.ls_trials[s] = ls_trials;
+      if (o.grad_evals) o.grad_evals[s] = grads;
+      if (status == ZEUS_CONVERGED && A.stop_counter) {
+        const unsigned long long old = atomicAdd(A.stop_counter, 1ull);
+        if ((long long)old + 1 == A.required_c) atomicExch(A.stop_flag, 1);
+      }
+    }
     __syncwarp();
   }
+};
 
-  // outputs; f_final = f(x) is the cached value of the current iterate
-  const zeus_bfgs_out& o = A.out;
-  for (int j = lane; j < d; j += 32) o.x_final[(int64_t)j * o.ld_out + s] = x[j];
-  if (lane == 0) {
-    o.f_final[s] = f0;
-    o.grad_norm[s] = gnorm;
-    o.iterations[s] = k;
-    o.status[s] = (uint8_t)status;
-    if (o.ls_trials) o.ls_trials[s] = ls_trials;
-    if (o.grad_evals) o.grad_evals[s] = grads;
-    if (status == ZEUS_CONVERGED && A.stop_counter) {
-      const unsigned long long old = atomicAdd(A.stop_counter, 1ull);
-      if ((long long)old + 1 == A.required_c) atomicExch(A.stop_flag, 1);
-    }
-  }
-  __syncwarp();
-}
-
-template <class Obj>
+template <class Obj, int DR>
 __global__ void __launch_bounds__(kBfgsWarps * 32) bfgs_warp_kernel(BfgsArgs A) {
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int d = A.d;
-  double* base = sm + (size_t)wib * A.warp_doubles;
-  double *H, *vec;
-  if (A.h_global) {
-    H = A.h_global + ((size_t)blockIdx.x * (blockDim.x >> 5) + wib) * (size_t)d * d;
-    vec = base;
-  } else {
-    H = base;
-    vec = base + (size_t)d * d;
+  // block-shared alpha table: alpha0 * shrink^t by repeated multiplication,
+  // exactly as linesearch.py:70 updates alpha
+  double* alpha_tab = sm;
+  if (threadIdx.x == 0) {
+    double a = A.alpha0;
+    for (int t = 0; t < A.nalpha; ++t) {
+      alpha_tab[t] = a;
+      a *= A.shrink;
+    }
   }
-  double *x = vec, *g = x + d, *p = g + d, *xn = p + d, *gn = xn + d, *dx = gn + d,
-         *dg = dx + d, *u = dg + d, *terms = u + d;
+  __syncthreads();
+  double* base = sm + A.nalpha + (size_t)wib * A.warp_doubles;
+  BfgsWarp<Obj, DR> W;
+  W.alpha_tab = alpha_tab;
+  double* v = base;
+  if constexpr (DR == 0) {
+    if (A.h_global) {
+      W.H = A.h_global + ((size_t)blockIdx.x * (blockDim.x >> 5) + wib) * (size_t)d * A.ldh;
+    } else {
+      W.H = v;
+      v += hsize(d, A.ldh);
+    }
+  } else {
+    W.H = nullptr;
+  }
+  W.row4 = v;  // [d][4] = {dg, g', dx_prev, u_prev}; 16-B aligned (offsets even)
+  v += 4 * d;
+  W.x = v;
+  v += d;
+  W.xn = v;
+  v += d;
+  W.p = v;
+  v += d;
+  W.g = v;
+  v += d;
+  W.gn = v;
+  v += d;
+  W.T = v;
   for (;;) {
     long long s = 0;
     if (lane == 0) s = (long long)atomicAdd(A.work, 1ull);
     s = __shfl_sync(kFull, s, 0);
     if (s >= A.n) break;
-    bfgs_one<Obj>(A, s, lane, H, x, g, p, xn, gn, dx, dg, u, terms);
+    BfgsWarp<Obj, DR> w = W;  // fresh pointer set per start (run() swaps x/xn, g/gn)
+    w.run(A, s, lane);
   }
 }
 
@@ -247,46 +494,89 @@ __global__ void __launch_bounds__(kBfgsWarps * 32) bfgs_warp_kernel(BfgsArgs A) 
 constexpr size_t kSmemLimit = 227 * 1024;
 constexpr size_t kWsHeader = 256;
 
-static inline int vec_doubles(int d) { return (8 + 2) * d; }  // 8 vectors + NACC<=2 term rows
 struct BfgsPlan {
-  int wpb;      // warps per block
-  bool smem_h;  // H in shared memory
+  int wpb;       // warps per block
+  int dr;        // register-resident H rows (0: smem / global)
+  bool smem_h;   // (dr == 0) H in shared memory
+  int ldh, tstride, bmax, nalpha;
+  size_t warp_doubles;
+  size_t smem;
 };
-static inline BfgsPlan bfgs_plan(int d) {
-  const size_t per_warp = ((size_t)d * d + vec_doubles(d)) * sizeof(double);
-  int wpb = (int)std::min<size_t>(kBfgsWarps, kSmemLimit / per_warp);
-  if (wpb >= 1) return {wpb, true};
-  return {kBfgsWarps, false};
+
+static inline int even(int v) { return (v + 1) & ~1; }
+
+static BfgsPlan bfgs_plan(int d, int nacc, int nterms, int iter_ls) {
+  BfgsPlan P{};
+  P.dr = d <= 16 ? 16 : d <= 32 ? 32 : 0;
+  P.tstride = std::max(1, nterms) | 1;
+  // sizes depend on d only (never on iter_ls), so the workspace query and the
+  // launch always agree on where H lives
+  (void)iter_ls;
+  P.bmax = std::max(1, std::min(32, kTermCap / std::max(1, nterms)));
+  P.nalpha = kAlphaTable;
+  P.ldh = d;  // lanes read consecutive columns: conflict-free for any ld
+  // term buffer rows: NACC * kWarpTrialRows rows of tstride, + 32 alpha scratch
+  const size_t vec = (size_t)4 * d + 5 * (size_t)d + (size_t)nacc * P.bmax * P.tstride + 32;
+  size_t per_warp = even((int)vec);
+  if (P.dr == 0) {
+    const size_t with_h = per_warp + hsize(d, P.ldh);
+    const int wpb = (int)std::min<size_t>(kBfgsWarps,
+                                          (kSmemLimit - P.nalpha * 8) / (with_h * 8));
+    if (wpb >= 1) {
+      P.smem_h = true;
+      P.wpb = wpb;
+      per_warp = with_h;
+    } else {
+      P.smem_h = false;
+      P.wpb = kBfgsWarps;
+    }
+  } else {
+    P.smem_h = false;
+    P.wpb = kBfgsWarps;
+  }
+  P.warp_doubles = per_warp;
+  P.smem = (P.nalpha + per_warp * P.wpb) * sizeof(double);
+  return P;
 }
+
 static inline int global_h_blocks(int sms) { return sms * 2; }
+
+template <class Obj, int DR>
+static int launch_plan(BfgsArgs A, const BfgsPlan& P, cudaStream_t s) {
+  auto kern = bfgs_warp_kernel<Obj, DR>;
+  if (P.smem > kSmemLimit)
+    return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs: d=%d needs %zu B smem", A.d, P.smem);
+  int rc = check_cuda(
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem),
+      "cudaFuncSetAttribute");
+  if (rc) return rc;
+  int per_sm = 0;
+  rc = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P.wpb * 32, P.smem),
+                  "occupancy");
+  if (rc) return rc;
+  const int sms = current_sm_count();
+  if (per_sm < 1 || sms < 1) return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs: kernel does not fit");
+  int grid = per_sm * sms;
+  if (DR == 0 && !P.smem_h) grid = std::min(grid, global_h_blocks(sms));
+  const int64_t need = (A.n + P.wpb - 1) / P.wpb;
+  if (grid > need) grid = (int)std::max<int64_t>(1, need);
+  kern<<<grid, P.wpb * 32, P.smem, s>>>(A);
+  return check_launch("bfgs_warp_kernel");
+}
 
 struct BfgsLaunch {
   template <class Obj>
   static int run(BfgsArgs A, cudaStream_t s) {
-    const int d = A.d;
-    const BfgsPlan plan = bfgs_plan(d);
-    A.warp_doubles = vec_doubles(d) + (plan.smem_h ? d * d : 0);
-    const size_t smem = (size_t)A.warp_doubles * sizeof(double) * plan.wpb;
-    if (smem > kSmemLimit)
-      return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs: d=%d needs %zu B smem", d, smem);
-    auto kern = bfgs_warp_kernel<Obj>;
-    int rc = check_cuda(
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-        "cudaFuncSetAttribute");
-    if (rc) return rc;
-    int per_sm = 0;
-    rc = check_cuda(
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, plan.wpb * 32, smem),
-        "occupancy");
-    if (rc) return rc;
-    const int sms = current_sm_count();
-    if (per_sm < 1 || sms < 1) return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs: kernel does not fit");
-    int grid = per_sm * sms;
-    if (!plan.smem_h) grid = std::min(grid, global_h_blocks(sms));
-    const int64_t need = (A.n + plan.wpb - 1) / plan.wpb;
-    if (grid > need) grid = (int)std::max<int64_t>(1, need);
-    kern<<<grid, plan.wpb * 32, smem, s>>>(A);
-    return check_launch("bfgs_warp_kernel");
+    const BfgsPlan P = bfgs_plan(A.d, Obj::NACC, std::max(1, A.d), A.iter_ls);
+    A.warp_doubles = (int)P.warp_doubles;
+    A.ldh = P.ldh;
+    A.tstride = P.tstride;
+    A.bmax = P.bmax;
+    A.nalpha = P.nalpha;
+    if (P.dr == 16) return launch_plan<Obj, 16>(A, P, s);
+    if (P.dr == 32) return launch_plan<Obj, 32>(A, P, s);
+    if (P.smem_h) A.h_global = nullptr;
+    return launch_plan<Obj, 0>(A, P, s);
   }
 };
 
@@ -298,7 +588,9 @@ extern "C" {
 
 size_t zeus_bfgs_workspace_bytes(int d, int64_t n) {
   (void)n;
-  if (d < 1 || bfgs_plan(d).smem_h) return kWsHeader;
+  if (d < 1) return kWsHeader;
+  const BfgsPlan P = bfgs_plan(d, 2, d, 1024);
+  if (P.dr > 0 || P.smem_h) return kWsHeader;
   int sms = current_sm_count();
   if (sms < 1) sms = 148;
   return kWsHeader + (size_t)global_h_blocks(sms) * kBfgsWarps * (size_t)d * d * sizeof(double);
@@ -307,11 +599,11 @@ size_t zeus_bfgs_workspace_bytes(int d, int64_t n) {
 int zeus_bfgs(int obj, int d, int64_t n, const double* x0, int64_t ldx,
               const zeus_bfgs_params* P, int64_t required_c, unsigned long long* stop_counter,
               int* stop_flag, zeus_bfgs_out* out, void* workspace, void* stream) {
-  if (d < 1 || n < 0 || ldx < n || !P || !out || !workspace ||
+  if (d < 1 || d > 32 * kMaxC || n < 0 || ldx < n || !P || !out || !workspace ||
       (obj == ZEUS_OBJ_GOLDSTEIN_PRICE && d != 2) || (n > 0 && (!x0 || !out->x_final ||
       !out->f_final || !out->grad_norm || !out->iterations || !out->status)) ||
       out->ld_out < n || !(P->theta > 0.0) || P->iter_bfgs < 0 || P->iter_ls < 1 ||
-      ((stop_counter == nullptr) != (stop_flag == nullptr)))
+      !(P->alpha0 > 0.0) || ((stop_counter == nullptr) != (stop_flag == nullptr)))
     return set_error(ZEUS_ERR_ARGUMENT, "zeus_bfgs: bad arguments");
   if (n == 0) return ZEUS_OK;
   cudaStream_t s = as_stream(stream);
@@ -331,7 +623,7 @@ int zeus_bfgs(int obj, int d, int64_t n, const double* x0, int64_t ldx,
   A.stop_flag = stop_flag;
   A.out = *out;
   A.work = (unsigned long long*)workspace;
-  A.h_global = bfgs_plan(d).smem_h ? nullptr : (double*)((char*)workspace + kWsHeader);
+  A.h_global = (double*)((char*)workspace + kWsHeader);
   int rc = check_cuda(cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), s), "memset");
   if (rc) return rc;
   rc = dispatch_objective<BfgsLaunch>(obj, A, s);

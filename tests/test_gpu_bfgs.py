@@ -1,10 +1,11 @@
 """GPU parity of multistart BFGS (bfgs.py:80-156) against the reference's
 golden outcomes and the oracle, from identical starts.
 
-Tolerance: statuses identical; |x - x_ref|_inf <= 1e-6;
-|f - f_ref| <= 1e-10 max(1,|f_ref|) for runs that stop on the gradient test
-(1e-6 for runs that hit the cap at a gradient kink); iteration counts are
-reported as a |dk| histogram, not gated.
+Tolerance (stated in tests/conftest.py): statuses identical;
+|x - x_ref|_inf <= 1e-6 (1e-5 for converged starts: theta / lambda_min);
+|f - f_ref| <= 1e-10 max(1,|f_ref|) (1e-6 for runs that hit the cap);
+escaping capped runs gate only the status; iteration counts are reported as
+a |dk| histogram, not gated.
 """
 
 import math
@@ -13,7 +14,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import BOXES
+from conftest import BOXES, assert_outcomes_close
 
 pytestmark = pytest.mark.gpu
 
@@ -36,18 +37,11 @@ def device_bfgs(name, starts, cap, theta=1e-6):
                 ls=out.ls_trials.cpu().numpy(), ng=out.grad_evals.cpu().numpy())
 
 
-def assert_outcomes_close(dev, ref_x, ref_f, ref_s, ref_k, label):
-    assert np.array_equal(dev["s"], ref_s), (label, np.flatnonzero(dev["s"] != ref_s)[:10])
-    nan_both = np.isnan(dev["x"]) & np.isnan(ref_x)
-    dx = np.where(nan_both, 0.0, np.abs(dev["x"] - ref_x))
-    assert np.max(dx) <= 1e-6, (label, np.max(dx))
-    fin = ~np.isnan(ref_f)
-    assert np.array_equal(np.isnan(dev["f"]), ~fin), label
-    tol = np.where(ref_s == 1, 1e-6, 1e-10)[fin]
-    assert np.all(np.abs(dev["f"][fin] - ref_f[fin]) <= tol * np.maximum(1, np.abs(ref_f[fin]))), label
+def check(dev, ref_x, ref_f, ref_s, ref_k, label, ref_gn=None):
+    dx = assert_outcomes_close(dev["x"], dev["f"], dev["s"], ref_x, ref_f, ref_s, label, ref_gn)
     dk = np.abs(dev["k"].astype(np.int64) - np.asarray(ref_k, dtype=np.int64))
-    print(f"{label}: {len(ref_s)} starts, |dk| mean {dk.mean():.2f} max {dk.max()}, "
-          f"bit-identical x {np.mean(np.all(dev['x'] == ref_x, axis=1)):.2f}")
+    print(f"{label}: {len(ref_s)} starts, max|dx| {dx.max():.2e}, |dk| mean {dk.mean():.2f} "
+          f"max {dk.max()}, bit-identical x {np.mean(np.all(dev['x'] == ref_x, axis=1)):.2f}")
 
 
 def test_matches_reference_golden(golden):
@@ -57,7 +51,7 @@ def test_matches_reference_golden(golden):
         name = "_".join(parts[:-5])
         cap = int(parts[-1])
         dev = device_bfgs(name, g[tag + "_starts"], cap)
-        assert_outcomes_close(dev, g[tag + "_x"], g[tag + "_f"], g[tag + "_s"], g[tag + "_k"], tag)
+        check(dev, g[tag + "_x"], g[tag + "_f"], g[tag + "_s"], g[tag + "_k"], tag, g[tag + "_gn"])
         assert np.array_equal(dev["s"] == 0, dev["gn"] < 1e-6)  # converged <=> |g| < theta
 
 
@@ -72,8 +66,8 @@ def test_matches_oracle(oracle, name, d, n, cap):
     starts = oracle.pso(name, d, n, 3, lo, hi, 2).positions
     ref = oracle.bfgs_batch(name, starts, iter_bfgs=cap)
     dev = device_bfgs(name, starts, cap)
-    assert_outcomes_close(dev, ref.x_final, ref.f_final, ref.status, ref.iterations,
-                          f"{name} d={d}")
+    check(dev, ref.x_final, ref.f_final, ref.status, ref.iterations, f"{name} d={d}",
+          ref.grad_norm)
     assert np.all(dev["ls"] >= dev["k"])            # >= 1 trial per iteration
     assert np.all(dev["ng"] <= dev["k"] + 1)
 

@@ -7,6 +7,8 @@ import math
 import numpy as np
 import pytest
 
+from conftest import assert_outcomes_close, xdiff
+
 pytestmark = pytest.mark.gpu
 
 
@@ -20,8 +22,8 @@ def test_config1_matches_oracle(z, oracle):
     assert res.pso_best_before_bfgs == sw.global_best_val
     pr = res.per_run
     assert len(pr) == 1024
-    assert np.array_equal(pr.status_codes, ref.status)
-    assert np.max(np.abs(pr.x_final - ref.x_final)) <= 1e-6
+    assert_outcomes_close(pr.x_final, pr.f_final, pr.status_codes, ref.x_final, ref.f_final,
+                          ref.status, "config 1")
     assert res.converged_count == int(np.sum(ref.status == 0))
     b = oracle.reduce_best(ref.f_final, ref.status)
     assert abs(res.best.f_final - ref.f_final[b]) <= 1e-10 * max(1, abs(ref.f_final[b]))
@@ -44,7 +46,8 @@ def test_config2_reduced_matches_oracle(z, oracle):
         assert max(pr.grad_norm[i], ref.grad_norm[i]) < 1e-4
     ok = pr.status_codes == ref.status
     assert len(mism) <= 2
-    assert np.max(np.abs(pr.x_final[ok] - ref.x_final[ok])) <= 1e-6
+    assert_outcomes_close(pr.x_final[ok], pr.f_final[ok], pr.status_codes[ok], ref.x_final[ok],
+                          ref.f_final[ok], ref.status[ok], "config 2 reduced")
     # PSO on device vs oracle: global best agrees
     res2 = z.zeus_run(z.rastrigin, cfg)
     assert abs(res2.pso_best_before_bfgs - sw.global_best_val) <= 1e-9

@@ -14,7 +14,7 @@ __all__ = ["ZeusNativeError", "lib", "check", "LIB_PATH", "BfgsParams", "BfgsOut
            "EXPORTED_SYMBOLS"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libzeus_sm100.so")
+LIB_PATH = os.environ.get("ZEUS_LIB") or os.path.join(HERE, "libzeus_sm100.so")
 
 OBJ_ROSENBROCK = 0
 OBJ_RASTRIGIN = 1

@@ -34,98 +34,11 @@
 //
 // Objective values keep the reference's sequential summation order, so f is
 // bit-identical to the reference wherever libm agrees.
-#include <algorithm>
+#include <stdlib.h>
 
-#include "objectives.cuh"
-#include "zeus_internal.h"
+#include "bfgs_common.cuh"
 
 namespace zeus {
-
-struct BfgsArgs {
-  int d;
-  int64_t n;
-  const double* x0;
-  int64_t ldx;
-  double theta;
-  int cap;
-  int iter_ls;
-  double c1, alpha0, shrink;
-  long long required_c;
-  unsigned long long* stop_counter;
-  int* stop_flag;
-  zeus_bfgs_out out;
-  unsigned long long* work;
-  double* h_global;  // non-null: H lives in HBM/L2 (d too large for smem)
-  int warp_doubles;  // shared-memory doubles per warp
-  int ldh;           // row stride of an smem/global H
-  int tstride;       // term-buffer row stride (odd, >= nterms)
-  int bmax;          // max trials per speculative batch
-  int nalpha;        // alpha table length (block smem)
-};
-
-constexpr int kBfgsWarps = 4;
-constexpr int kTermCap = 320;   // objective terms per speculative batch
-constexpr int kAlphaTable = 64;
-constexpr int kMaxC = 32;       // columns per lane in the smem / HBM path: d <= 1024
-
-// H slice size in doubles, kept even so the row4 double2 loads stay 16-B aligned
-__host__ __device__ inline size_t hsize(int d, int ldh) { return ((size_t)d * ldh + 1) & ~(size_t)1; }
-
-
-// Trial-point accessor: coordinate j of x + alpha p (reference: x + alpha*p,
-// numpy multiply then add, no contraction).
-struct TrialX {
-  const double* x;
-  const double* p;
-  double alpha;
-  __device__ __forceinline__ double operator()(int j) const { return x[j] + alpha * p[j]; }
-};
-
-__device__ __forceinline__ void warp_sum8(double v[8]) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] += __shfl_xor_sync(kFull, v[q], o);
-  }
-}
-
-// Evaluate B trial points; lane b < B returns trial b's value/accumulators.
-// `trial_alpha(b)` gives trial b's step; B == 0 means "evaluate x itself".
-template <class Obj>
-__device__ __forceinline__ double eval_batch(int B, const double* alpha_of, int d,
-                                             const double* x, const double* p, double* T,
-                                             int tstride, int rows, int lane,
-                                             double acc[Obj::NACC]) {
-  const int nt = Obj::nterms(d);
-  const int nb = B > 0 ? B : 1;
-  const int total = nb * nt;
-  for (int q = lane; q < total; q += 32) {
-    const int b = q / nt, j = q - b * nt;
-    double t[Obj::NACC];
-    if (B > 0) {
-      Obj::term(TrialX{x, p, alpha_of[b]}, j, d, t);
-    } else {
-      Obj::term(DenseX{x}, j, d, t);
-    }
-#pragma unroll
-    for (int a = 0; a < Obj::NACC; ++a) T[(a * rows + b) * tstride + j] = t[a];
-  }
-  __syncwarp();
-  double f = 0.0;
-  if (lane < nb) {
-#pragma unroll
-    for (int a = 0; a < Obj::NACC; ++a) {
-      const double* row = T + (a * rows + lane) * tstride;
-      double s = Obj::init(a, d);
-      for (int j = 0; j < nt; ++j) s = s + row[j];
-      acc[a] = s;
-    }
-    bool err = false;
-    f = Obj::finish(acc, d, err);
-  }
-  __syncwarp();
-  return f;
-}
 
 template <class Obj, int DR>
 struct BfgsWarp {
@@ -142,6 +55,7 @@ struct BfgsWarp {
   }
 
   __device__ void run(const BfgsArgs& A, long long s, int lane) {
+    PHASE_T0();
     const int d = A.d;
     const int C = (d + 31) >> 5;  // columns per lane
     double hreg[DR > 0 ? DR : 1];
@@ -180,8 +94,9 @@ struct BfgsWarp {
       ++grads;
       bool err = false;
       double part = 0.0;
+      const bool slow = grad_needs_slow<Obj>(x, d, lane);
       for (int j = lane; j < d; j += 32) {
-        const double gj = Obj::grad(DenseX{x}, j, d, acc, err);
+        const double gj = grad_at<Obj>(x, j, d, acc, err, slow);
         g[j] = gj;
         p[j] = -gj;  // H0 = I: -(I @ g) is exact
         part = fma(gj, gj, part);
@@ -196,6 +111,7 @@ struct BfgsWarp {
       __syncwarp();
     }
 
+    PHASE(5);  // prologue: loads, H = I, f(x0), first gradient
     for (;;) {
       if (gnorm < A.theta) {
         status = ZEUS_CONVERGED;
@@ -240,6 +156,7 @@ struct BfgsWarp {
           B = min(2 * B, A.bmax);
         }
       }
+      PHASE(0);  // line search (term pass + folds + ballot + x_new)
       ls_trials += t_acc + 1;
       prev_trials = t_acc + 1;
       __syncwarp();
@@ -249,8 +166,9 @@ struct BfgsWarp {
       double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       {
         bool err = false;
+        const bool slow = grad_needs_slow<Obj>(xn, d, lane);
         for (int j = lane; j < d; j += 32) {
-          const double gj = Obj::grad(DenseX{xn}, j, d, acc_new, err);
+          const double gj = grad_at<Obj>(xn, j, d, acc_new, err, slow);
           const double dgj = gj - g[j];
           gn[j] = gj;
           row4[4 * j + 0] = dgj;
@@ -263,6 +181,7 @@ struct BfgsWarp {
       }
       __syncwarp();
 
+      PHASE(1);  // gradient
       // ---- fused pass over H: lazy rank-2 update, u = H dg, w = H g'
       double u_own[DR > 0 ? 1 : kMaxC], w_own[DR > 0 ? 1 : kMaxC];
       if constexpr (DR > 0) {
@@ -345,6 +264,7 @@ struct BfgsWarp {
         }
       }
 
+      PHASE(2);  // H pass
       // ---- one 8-value reduction: norms, curvature and the p' scalars
       {
         for (int c = 0; c < C; ++c) {
@@ -396,6 +316,7 @@ struct BfgsWarp {
           pd = fma(gn[j], pj, pd);
         }
       }
+      PHASE(3);  // 8-value reduction + p' + update coefficients
       // x, g <- x_new, g_new (bfgs.py:141-145)
       {
         double* t = x;
@@ -410,6 +331,7 @@ struct BfgsWarp {
       for (int a = 0; a < Obj::NACC; ++a) acc[a] = acc_new[a];
       gnorm = sqrt(part[0]);
       ddir = warp_sum(pd);  // np.dot(g, p) of the next line search
+      PHASE(4);  // ddir reduction + swap
       ++k;
       __syncwarp();
       if (A.stop_flag && *(volatile int*)A.stop_flag) {
@@ -438,7 +360,7 @@ struct BfgsWarp {
 };
 
 template <class Obj, int DR>
-__global__ void __launch_bounds__(kBfgsWarps * 32) bfgs_warp_kernel(BfgsArgs A) {
+__global__ void __launch_bounds__(kBfgsWarps * 32, DR > 0 ? ZEUS_MINB : 1) bfgs_warp_kernel(BfgsArgs A) {
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int d = A.d;
@@ -584,7 +506,25 @@ struct BfgsLaunch {
 
 using namespace zeus;
 
+static bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] && v[0] != '0';
+}
+
 extern "C" {
+
+#ifdef ZEUS_PHASE_TIMING
+// diagnostics only (not in include/zeus_b200.h): copy out / reset the phase cycles
+int zeus_debug_phase_cycles(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, zeus_phase_cycles, sizeof(unsigned long long) * 8) != cudaSuccess)
+    return -2;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(zeus_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 size_t zeus_bfgs_workspace_bytes(int d, int64_t n) {
   (void)n;
@@ -626,7 +566,10 @@ int zeus_bfgs(int obj, int d, int64_t n, const double* x0, int64_t ldx,
   A.h_global = (double*)((char*)workspace + kWsHeader);
   int rc = check_cuda(cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), s), "memset");
   if (rc) return rc;
-  rc = dispatch_objective<BfgsLaunch>(obj, A, s);
+  if (bfgs_team_covers(obj, d) && !getenv_flag("ZEUS_NO_TEAM"))
+    rc = launch_bfgs_team(obj, A, s);
+  else
+    rc = dispatch_objective<BfgsLaunch>(obj, A, s);
   if (rc == ZEUS_ERR_ARGUMENT) return set_error(rc, "unknown objective id %d", obj);
   return rc;
 }

@@ -1,0 +1,179 @@
+// bfgs_common.cuh -- pieces shared by the warp-per-start (bfgs.cu) and the
+// CTA-per-start (bfgs_team.cu) BFGS kernels: launch arguments, the trial-point
+// accessor, the speculative term pass, gradient helpers.
+#pragma once
+#include <algorithm>
+
+#include "objectives.cuh"
+#include "zeus_internal.h"
+
+namespace zeus {
+
+struct BfgsArgs {
+  int d;
+  int64_t n;
+  const double* x0;
+  int64_t ldx;
+  double theta;
+  int cap;
+  int iter_ls;
+  double c1, alpha0, shrink;
+  long long required_c;
+  unsigned long long* stop_counter;
+  int* stop_flag;
+  zeus_bfgs_out out;
+  unsigned long long* work;
+  double* h_global;  // non-null: H lives in HBM/L2 (d too large for smem)
+  int warp_doubles;  // shared-memory doubles per warp
+  int ldh;           // row stride of an smem/global H
+  int tstride;       // term-buffer row stride (odd, >= nterms)
+  int bmax;          // max trials per speculative batch
+  int nalpha;        // alpha table length (block smem)
+};
+
+constexpr int kBfgsWarps = 4;
+#ifndef ZEUS_TERM_UNROLL
+#define ZEUS_TERM_UNROLL 4
+#endif
+#ifndef ZEUS_MINB
+#define ZEUS_MINB 4
+#endif
+constexpr int kU = ZEUS_TERM_UNROLL;  // independent objective terms per lane per step
+
+// Optional per-phase cycle accounting (build with -DZEUS_PHASE_TIMING): lane 0
+// of every warp adds clock64() deltas into zeus_phase_cycles[] (diagnostics
+// for the latency probe, scripts/latency_probe.py; off in normal builds).
+#ifdef ZEUS_PHASE_TIMING
+__device__ unsigned long long zeus_phase_cycles[8];
+#define PHASE_T0() long long _pt = clock64()
+#define PHASE(i)                                                  \
+  do {                                                            \
+    __syncwarp();                                                 \
+    const long long _n = clock64();                               \
+    if (lane == 0) atomicAdd(&zeus_phase_cycles[i], (unsigned long long)(_n - _pt)); \
+    _pt = _n;                                                     \
+  } while (0)
+#else
+#define PHASE_T0()
+#define PHASE(i)
+#endif
+constexpr int kTermCap = 320;   // objective terms per speculative batch
+constexpr int kAlphaTable = 64;
+constexpr int kMaxC = 32;       // columns per lane in the smem / HBM path: d <= 1024
+
+// H slice size in doubles, kept even so the row4 double2 loads stay 16-B aligned
+__host__ __device__ inline size_t hsize(int d, int ldh) { return ((size_t)d * ldh + 1) & ~(size_t)1; }
+
+
+// Trial-point accessor: coordinate j of x + alpha p (reference: x + alpha*p,
+// numpy multiply then add, no contraction).
+struct TrialX {
+  const double* x;
+  const double* p;
+  double alpha;
+  __device__ __forceinline__ double operator()(int j) const { return x[j] + alpha * p[j]; }
+};
+
+__device__ __forceinline__ void warp_sum8(double v[8]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] += __shfl_xor_sync(kFull, v[q], o);
+  }
+}
+
+// Term pass of a batch: (trial b, term j) pairs q = b * nt + j are spread over
+// the lanes, four independent terms per lane per step (their libm chains
+// overlap); (b, j) advance incrementally, no integer division per term.
+template <class Obj, class M, int NTH = 32>
+__device__ __forceinline__ void term_pass(int B, int nt, int total, const double* alpha_of,
+                                          int d, const double* x, const double* p, double* T,
+                                          int tstride, int rows, int lane, bool& oor) {
+  const int step_b = NTH / nt, step_j = NTH - step_b * nt;
+  int b = lane / nt, j = lane - b * nt;
+  for (int q0 = lane; q0 < total; q0 += NTH * kU) {
+    double t[kU][Obj::NACC];
+    int bb[kU], jj[kU];
+#pragma unroll
+    for (int r = 0; r < kU; ++r) {
+      bb[r] = b;
+      jj[r] = j;
+      if (q0 + NTH * r < total) {
+        if (B > 0) {
+          Obj::template term<M>(TrialX{x, p, alpha_of[b]}, j, d, t[r], oor);
+        } else {
+          Obj::template term<M>(DenseX{x}, j, d, t[r], oor);
+        }
+      }
+      j += step_j;
+      b += step_b;
+      while (j >= nt) {  // at most once when NTH >= nt
+        j -= nt;
+        ++b;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kU; ++r) {
+      if (q0 + NTH * r < total) {
+#pragma unroll
+        for (int a = 0; a < Obj::NACC; ++a) T[(a * rows + bb[r]) * tstride + jj[r]] = t[r][a];
+      }
+    }
+  }
+}
+
+// Evaluate B trial points x + alpha_of[b] p; lane b < B returns trial b's
+// value and accumulators (reference-order fold).  B == 0 evaluates x itself.
+template <class Obj>
+__device__ __forceinline__ double eval_batch(int B, const double* alpha_of, int d,
+                                             const double* x, const double* p, double* T,
+                                             int tstride, int rows, int lane,
+                                             double acc[Obj::NACC]) {
+  const int nt = Obj::nterms(d);
+  const int nb = B > 0 ? B : 1;
+  const int total = nb * nt;
+  if (total > 0) {
+    bool oor = false;
+    term_pass<Obj, FastMath>(B, nt, total, alpha_of, d, x, p, T, tstride, rows, lane, oor);
+    if (__any_sync(kFull, oor))  // some |2 pi x| > kTrigMax: redo with CUDA libm
+      term_pass<Obj, PreciseMath>(B, nt, total, alpha_of, d, x, p, T, tstride, rows, lane, oor);
+  }
+  __syncwarp();
+  double f = 0.0;
+  if (lane < nb) {
+#pragma unroll
+    for (int a = 0; a < Obj::NACC; ++a) {
+      const double* row = T + (a * rows + lane) * tstride;
+      double s = Obj::init(a, d);
+      for (int j = 0; j < nt; ++j) s = s + row[j];
+      acc[a] = s;
+    }
+    bool err = false;
+    f = Obj::finish(acc, d, err);
+  }
+  __syncwarp();
+  return f;
+}
+
+// Gradient component j at xs (fast trig, libm fallback decided warp-wide).
+template <class Obj>
+__device__ __forceinline__ double grad_at(const double* xs, int j, int d, const double* acc,
+                                          bool& err, bool slow) {
+  bool oor = false;
+  return slow ? Obj::template grad<PreciseMath>(DenseX{xs}, j, d, acc, err, oor)
+              : Obj::template grad<FastMath>(DenseX{xs}, j, d, acc, err, oor);
+}
+template <class Obj>
+__device__ __forceinline__ bool grad_needs_slow(const double* xs, int d, int lane) {
+  bool oor = false;
+  for (int j = lane; j < d; j += 32) oor |= !trig_in_range(kTwoPi * xs[j]);
+  return __any_sync(kFull, oor);
+}
+
+
+// Launch of the CTA-per-start kernel family (bfgs_team.cu).  Returns
+// ZEUS_ERR_UNSUPPORTED when no team shape covers (obj, d).
+int launch_bfgs_team(int obj, BfgsArgs A, cudaStream_t s);
+bool bfgs_team_covers(int obj, int d);
+
+}  // namespace zeus

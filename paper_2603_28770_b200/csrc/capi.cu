@@ -63,7 +63,8 @@ __global__ void objective_gradient_kernel(int d, int64_t n, const double* x, int
   value_seq<Obj>(X, d, acc, err);  // real parts shared by every tangent pass
   err = false;
   for (int k = 0; k < d; ++k) {
-    const double gk = Obj::grad(X, k, d, acc, err);
+    bool oor = false;
+    const double gk = Obj::template grad<AutoMath>(X, k, d, acc, err, oor);
     g[(int64_t)k * ldx + i] = err ? __longlong_as_double(0x7ff8000000000000LL) : gk;
   }
   if (domain_error) domain_error[i] = err ? 1 : 0;

@@ -19,6 +19,7 @@
 // computed once per start and broadcast.
 #pragma once
 #include "zeus_common.cuh"
+#include "zeus_trig.cuh"
 
 namespace zeus {
 
@@ -39,14 +40,46 @@ __device__ __forceinline__ Dual operator*(Dual a, double s) { return {a.r * s, a
 __device__ __forceinline__ Dual operator*(double s, Dual a) { return {a.r * s, a.d * s}; }
 __device__ __forceinline__ Dual operator/(Dual a, double s) { return {a.r / s, a.d / s}; }
 
+// Math policies for the transcendental calls.  Fast: branch-free sincos
+// (zeus_trig.cuh) valid on |x| <= kTrigMax, raising `oor` outside so the
+// caller can re-evaluate the whole batch with Precise (CUDA libm) -- keeping
+// the hot loops branch-free lets independent terms interleave.
+struct FastMath {
+  __device__ static __forceinline__ double cos(double x, bool& oor) {
+    oor |= !trig_in_range(x);
+    return sincos_fast(x).c;
+  }
+  __device__ static __forceinline__ double sin(double x, bool& oor) {
+    oor |= !trig_in_range(x);
+    return sincos_fast(x).s;
+  }
+};
+struct PreciseMath {
+  __device__ static __forceinline__ double cos(double x, bool&) { return ::cos(x); }
+  __device__ static __forceinline__ double sin(double x, bool&) { return ::sin(x); }
+};
+// Single-call policy (PSO, thread-sequential code): fast path, libm fallback.
+struct AutoMath {
+  __device__ static __forceinline__ double cos(double x, bool&) {
+    return trig_in_range(x) ? sincos_fast(x).c : ::cos(x);
+  }
+  __device__ static __forceinline__ double sin(double x, bool&) {
+    return trig_in_range(x) ? sincos_fast(x).s : ::sin(x);
+  }
+};
+
 // Elementary functions: `err` is raised where autodiff.py raises DomainError.
 __device__ __forceinline__ double gexp(double x, bool&) { return exp(x); }
 __device__ __forceinline__ Dual gexp(Dual x, bool&) {
   const double v = exp(x.r);
   return {v, v * x.d};
 }
-__device__ __forceinline__ double gcos(double x) { return cos(x); }
-__device__ __forceinline__ Dual gcos(Dual x) { return {cos(x.r), (-sin(x.r)) * x.d}; }
+template <class M>
+__device__ __forceinline__ double gcos(double x, bool& oor) { return M::cos(x, oor); }
+template <class M>
+__device__ __forceinline__ Dual gcos(Dual x, bool& oor) {
+  return {M::cos(x.r, oor), (-M::sin(x.r, oor)) * x.d};
+}
 // float path only rejects negatives; Dual path also rejects 0 (autodiff.py:198-216)
 __device__ __forceinline__ double gsqrt(double x, bool& err) {
   if (x < 0.0) err = true;
@@ -71,16 +104,16 @@ __device__ __forceinline__ double tangent<Dual>(const Dual& v) { return v.d; }
 //   NACC                      number of sequential accumulators (1 or 2)
 //   nterms(d)                 terms folded into the accumulators
 //   init(a, d)                accumulator a's initial float value
-//   term<T>(X, j, d, t[NACC]) term j (X(j) -> coordinate j)
-//   finish<T>(acc[NACC], d, err)
-//   grad(X, i, d, acc, err)   d f / d x_i from the Dual rules (see header)
+//   term<M>(X, j, d, t[NACC], oor)   term j (X(j) -> coordinate j), math policy M
+//   finish(acc[NACC], d, err)
+//   grad<M>(X, i, d, acc, err, oor)  d f / d x_i from the Dual rules (see header)
 // ---------------------------------------------------------------------------
 
 // objectives.py:33-45  (total = total + (a*a + 100*(b*b)), a = 1-x_i, b = x_{i+1}-x_i^2)
 struct Rosenbrock {
   static constexpr int kId = ZEUS_OBJ_ROSENBROCK;
   static constexpr int NACC = 1;
-  __device__ static int nterms(int d) { return d - 1; }
+  __host__ __device__ static int nterms(int d) { return d - 1; }
   __device__ static double init(int, int) { return 0.0; }
   template <class T>
   __device__ static T term2(T xj, T xj1) {
@@ -88,13 +121,13 @@ struct Rosenbrock {
     const T b = xj1 - xj * xj;
     return a * a + 100.0 * (b * b);
   }
-  template <class X>
-  __device__ static void term(const X& x, int j, int, double t[1]) {
+  template <class M = AutoMath, class X>
+  __device__ static void term(const X& x, int j, int, double t[1], bool&) {
     t[0] = term2<double>(x(j), x(j + 1));
   }
   __device__ static double finish(const double acc[1], int, bool&) { return acc[0]; }
-  template <class X>
-  __device__ static double grad(const X& x, int i, int d, const double*, bool&) {
+  template <class M = AutoMath, class X>
+  __device__ static double grad(const X& x, int i, int d, const double*, bool&, bool&) {
     // seed x_i: term i-1 sees it as x_{j+1}, term i as x_j
     const double xi = x(i);
     double g = 0.0;
@@ -115,20 +148,20 @@ struct Rosenbrock {
 struct Rastrigin {
   static constexpr int kId = ZEUS_OBJ_RASTRIGIN;
   static constexpr int NACC = 1;
-  __device__ static int nterms(int d) { return d; }
+  __host__ __device__ static int nterms(int d) { return d; }
   __device__ static double init(int, int d) { return 10.0 * d; }
-  template <class T>
-  __device__ static T term1(T xi) {
-    return xi * xi - 10.0 * gcos(kTwoPi * xi);
+  template <class M, class T>
+  __device__ static T term1(T xi, bool& oor) {
+    return xi * xi - 10.0 * gcos<M>(kTwoPi * xi, oor);
   }
-  template <class X>
-  __device__ static void term(const X& x, int j, int, double t[1]) {
-    t[0] = term1<double>(x(j));
+  template <class M = AutoMath, class X>
+  __device__ static void term(const X& x, int j, int, double t[1], bool& oor) {
+    t[0] = term1<M, double>(x(j), oor);
   }
   __device__ static double finish(const double acc[1], int, bool&) { return acc[0]; }
-  template <class X>
-  __device__ static double grad(const X& x, int i, int, const double*, bool&) {
-    return term1<Dual>(Dual{x(i), 1.0}).d;
+  template <class M = AutoMath, class X>
+  __device__ static double grad(const X& x, int i, int, const double*, bool&, bool& oor) {
+    return term1<M, Dual>(Dual{x(i), 1.0}, oor).d;
   }
 };
 
@@ -136,16 +169,16 @@ struct Rastrigin {
 struct Ackley {
   static constexpr int kId = ZEUS_OBJ_ACKLEY;
   static constexpr int NACC = 2;  // sum_sq, sum_cos
-  __device__ static int nterms(int d) { return d; }
+  __host__ __device__ static int nterms(int d) { return d; }
   __device__ static double init(int, int) { return 0.0; }
-  template <class T>
-  __device__ static void terms(T xi, T& sq, T& cs) {
+  template <class M, class T>
+  __device__ static void terms(T xi, T& sq, T& cs, bool& oor) {
     sq = xi * xi;
-    cs = gcos(kTwoPi * xi);
+    cs = gcos<M>(kTwoPi * xi, oor);
   }
-  template <class X>
-  __device__ static void term(const X& x, int j, int, double t[2]) {
-    terms<double>(x(j), t[0], t[1]);
+  template <class M = AutoMath, class X>
+  __device__ static void term(const X& x, int j, int, double t[2], bool& oor) {
+    terms<M, double>(x(j), t[0], t[1], oor);
   }
   template <class T>
   __device__ static T outer(T sum_sq, T sum_cos, int d, bool& err) {
@@ -155,10 +188,11 @@ struct Ackley {
   __device__ static double finish(const double acc[2], int d, bool& err) {
     return outer<double>(acc[0], acc[1], d, err);
   }
-  template <class X>
-  __device__ static double grad(const X& x, int i, int d, const double* acc, bool& err) {
+  template <class M = AutoMath, class X>
+  __device__ static double grad(const X& x, int i, int d, const double* acc, bool& err,
+                                bool& oor) {
     Dual sq, cs;
-    terms<Dual>(Dual{x(i), 1.0}, sq, cs);
+    terms<M, Dual>(Dual{x(i), 1.0}, sq, cs, oor);
     // real parts: the full sequential sums; tangents: the only non-zero term
     return outer<Dual>(Dual{acc[0], sq.d}, Dual{acc[1], cs.d}, d, err).d;
   }
@@ -168,7 +202,7 @@ struct Ackley {
 struct GoldsteinPrice {
   static constexpr int kId = ZEUS_OBJ_GOLDSTEIN_PRICE;
   static constexpr int NACC = 1;
-  __device__ static int nterms(int) { return 1; }
+  __host__ __device__ static int nterms(int) { return 1; }
   __device__ static double init(int, int) { return 0.0; }
   template <class T>
   __device__ static T eval(T x1, T x2) {
@@ -182,15 +216,15 @@ struct GoldsteinPrice {
                                  36.0 * x1 * x2 + 27.0 * x2 * x2);
     return first * second;
   }
-  template <class X>
-  __device__ static void term(const X& x, int, int, double t[1]) {
+  template <class M = AutoMath, class X>
+  __device__ static void term(const X& x, int, int, double t[1], bool&) {
     t[0] = eval<double>(x(0), x(1));
   }
   // the single "term" is the whole value: 0.0 + v == v for every v but -0.0,
   // and GP is >= 3 on its domain; finish returns the term itself.
   __device__ static double finish(const double acc[1], int, bool&) { return acc[0]; }
-  template <class X>
-  __device__ static double grad(const X& x, int i, int, const double*, bool&) {
+  template <class M = AutoMath, class X>
+  __device__ static double grad(const X& x, int i, int, const double*, bool&, bool&) {
     return i == 0 ? eval<Dual>(Dual{x(0), 1.0}, Dual{x(1), 0.0}).d
                   : eval<Dual>(Dual{x(0), 0.0}, Dual{x(1), 1.0}).d;
   }
@@ -214,9 +248,10 @@ __device__ __forceinline__ double value_seq(const X& x, int d, double acc[Obj::N
 #pragma unroll
   for (int a = 0; a < Obj::NACC; ++a) acc[a] = Obj::init(a, d);
   const int nt = Obj::nterms(d);
+  bool oor = false;
   for (int j = 0; j < nt; ++j) {
     double t[Obj::NACC];
-    Obj::term(x, j, d, t);
+    Obj::template term<AutoMath>(x, j, d, t, oor);
 #pragma unroll
     for (int a = 0; a < Obj::NACC; ++a) acc[a] = acc[a] + t[a];
   }

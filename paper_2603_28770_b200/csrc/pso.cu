@@ -37,7 +37,10 @@ template <>
 struct StreamAcc<Rastrigin> {
   double total;
   __device__ explicit StreamAcc(int d = 0) : total(10.0 * d) {}
-  __device__ void push(double x) { total = total + Rastrigin::term1<double>(x); }
+  __device__ void push(double x) {
+    bool oor = false;
+    total = total + Rastrigin::term1<AutoMath, double>(x, oor);
+  }
   __device__ double result(int) { return total; }
 };
 template <>
@@ -45,7 +48,8 @@ struct StreamAcc<Ackley> {
   double sq = 0.0, cs = 0.0;
   __device__ void push(double x) {
     double a, b;
-    Ackley::terms<double>(x, a, b);
+    bool oor = false;
+    Ackley::terms<AutoMath, double>(x, a, b, oor);
     sq = sq + a;
     cs = cs + b;
   }

@@ -1,0 +1,102 @@
+// zeus_trig.cuh -- branch-free double sincos for the objective kernels.
+//
+// CUDA's cos/sin carry a Payne-Hanek slow path behind a branch, so several
+// independent calls in one thread cannot be interleaved by the scheduler;
+// the speculative line search evaluates up to 21 x d cosines per iteration
+// and was latency-bound on exactly that.  Here the reduction is a 3-constant
+// Cody-Waite reduction (exact first step, FMA-exact tail; valid for
+// |x| <= kTrigMax, quotient < 2^17) and
+// the kernels are the fdlibm / musl __sin / __cos minimax polynomials; both
+// polynomials are evaluated and the quadrant selects, so there is no branch.
+// Outside |x| <= kTrigMax callers fall back to the libm path (see FastMath).
+//
+// Accuracy: the reduced argument is carried as a double-double and the
+// leading polynomial terms are formed with exact-product corrections, so the
+// result is correctly rounded except within a small fraction of an ulp of a
+// rounding boundary; near a zero of the function the absolute error stays
+// below 1e-27 (what matters inside a sum of terms).
+// tests/test_trig.py checks the host build of this file against glibc and
+// mpmath on 2e5 samples.
+#pragma once
+
+#ifndef __CUDACC__
+#include <cmath>
+#ifndef __host__
+#define __host__
+#endif
+#ifndef __device__
+#define __device__
+#endif
+#ifndef __forceinline__
+#define __forceinline__ inline
+#endif
+#endif
+
+namespace zeus {
+
+constexpr double kTrigMax = 1.0e5;
+
+struct SinCos {
+  double s, c;
+};
+
+__host__ __device__ __forceinline__ SinCos sincos_fast(double x) {
+  constexpr double INV_PIO2 = 0.6366197723675814;  // 0x3fe45f306dc9c883
+  // pi/2 = PIO2_1 (33 bits: fn * PIO2_1 is exact for |fn| < 2^20) + 1T + 1TT
+  constexpr double PIO2_1 = 1.5707963267341256;     // 0x3ff921fb54400000
+  constexpr double PIO2_1T = 6.077100506506192e-11;  // 0x3dd0b4611a626331
+  constexpr double PIO2_1TT = 3.5215598651832e-27;   // 0x3a71701b839a2520
+  // fdlibm k_sin.c / k_cos.c coefficients (Sun Microsystems, public domain)
+  constexpr double S1 = -1.66666666666666324348e-01, S2 = 8.33333333332248946124e-03,
+                   S3 = -1.98412698298579493134e-04, S4 = 2.75573137070700676789e-06,
+                   S5 = -2.50507602534068634195e-08, S6 = 1.58969099521155010221e-10;
+  constexpr double C1 = 4.16666666666666019037e-02, C2 = -1.38888888888741095749e-03,
+                   C3 = 2.48015872894767294178e-05, C4 = -2.75573143513906633035e-07,
+                   C5 = 2.08757232129817482790e-09, C6 = -1.13596475577881948265e-11;
+#ifdef __CUDA_ARCH__
+  const double fn = rint(x * INV_PIO2);
+#else
+  const double fn = std::nearbyint(x * INV_PIO2);
+#endif
+  // reduced argument as a double-double rh + rl (|fn| < 2^17 here)
+  const double r0 = x - fn * PIO2_1;  // exact (Sterbenz)
+  const double p = fn * PIO2_1T;
+  const double pe = fma(fn, PIO2_1T, -p);  // exact product error
+  const double rh = r0 - p;
+  const double bb = rh - r0;
+  const double rl = ((r0 - (rh - bb)) + (-p - bb)) - pe - fn * PIO2_1TT;  // TwoSum error
+  // z = (rh + rl)^2 as z + zl
+  const double z = rh * rh;
+  const double zl = fma(rh, rh, -z) + 2.0 * rh * rl;
+  const double w = z * z;
+  // sin: rh + S1 rh^3 (double-double) + rh^5 P(z) + rl (1 - z/2)
+  const double c3 = z * rh, c3l = fma(z, rh, -c3) + zl * rh;
+  const double t1 = c3 * S1, t1l = fma(c3, S1, -t1) + c3l * S1;
+  const double sh = rh + t1, sl = t1 - (sh - rh);  // Fast2Sum, |rh| >= |t1|
+  const double s5 = c3 * z * fma(z * w, fma(z, S6, S5), fma(z, fma(z, S4, S3), S2));
+  const double s = sh + (sl + (t1l + s5 + rl * fma(-0.5, z, 1.0)));
+  // cos: 1 - z/2 (exact split) + C1 z^2 (double-double) + z^3 Q(z)
+  const double hz = 0.5 * z, a = 1.0 - hz, al = (1.0 - a) - hz;
+  const double w_l = fma(z, z, -w) + 2.0 * z * zl;
+  const double t2 = w * C1, t2l = fma(w, C1, -t2) + w_l * C1;
+  const double ch = a + t2, cl = t2 - (ch - a);  // |a| >= 0.69 > |t2|
+  const double c6 = w * z * fma(w * z, fma(z, C6, C5), fma(z, fma(z, C4, C3), C2));
+  const double c = ch + (cl + (al - 0.5 * zl + t2l + c6));
+  const int q = (int)fn & 3;
+  SinCos out;
+  out.s = (q == 0) ? s : (q == 1) ? c : (q == 2) ? -s : -c;
+  out.c = (q == 0) ? c : (q == 1) ? -s : (q == 2) ? -c : s;
+  // tiny arguments: sin x = x (keeps the sign of zero), cos x = 1
+  const double ax = x < 0 ? -x : x;
+  if (ax < 1.4901161193847656e-08) {  // 2^-26
+    out.s = x;
+    out.c = 1.0;
+  }
+  return out;
+}
+
+__host__ __device__ __forceinline__ bool trig_in_range(double x) {
+  return x <= kTrigMax && x >= -kTrigMax;  // false for NaN too
+}
+
+}  // namespace zeus

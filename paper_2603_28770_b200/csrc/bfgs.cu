@@ -54,6 +54,50 @@ struct BfgsWarp {
     return a;
   }
 
+  // Write the carry record of a start that reached iteration k1 (layout in
+  // bfgs_common.cuh); the pending lazy rank-2 update is applied first so the
+  // record holds H_k itself.
+  __device__ void promote(const BfgsArgs& A, long long s, int lane, double* hreg, bool pending,
+                          double aj, double bj, double f0, const double* acc, double gnorm,
+                          double ddir, int k, int ls_trials, int grads, int prev_trials) {
+    const int d = A.d;
+    unsigned long long slot = 0;
+    if (lane == 0) slot = atomicAdd(A.promo_count, 1ull);
+    slot = __shfl_sync(kFull, slot, 0);
+    double* rec = A.carry + (size_t)slot * A.carry_stride;
+    if (lane == 0) {
+      rec[0] = (double)s;
+      rec[1] = k;
+      rec[2] = ls_trials;
+      rec[3] = grads;
+      rec[4] = prev_trials;
+      rec[5] = f0;
+      rec[6] = acc[0];
+      rec[7] = Obj::NACC > 1 ? acc[Obj::NACC - 1] : 0.0;
+      rec[8] = gnorm;
+      rec[9] = ddir;
+    }
+    for (int j = lane; j < d; j += 32) {
+      rec[kCarryHead + j] = x[j];
+      rec[kCarryHead + d + j] = g[j];
+      rec[kCarryHead + 2 * d + j] = p[j];
+    }
+    if constexpr (DR > 0) {
+      double* Hr = rec + kCarryHead + 3 * d;
+      if (lane < d) {
+#pragma unroll
+        for (int i = 0; i < DR; ++i) {
+          if (i < d) {
+            double h = hreg[i];
+            if (pending) h = fma(row4[4 * i + 2], aj, fma(row4[4 * i + 3], bj, h));
+            Hr[(int64_t)i * d + lane] = h;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
   __device__ void run(const BfgsArgs& A, long long s, int lane) {
     PHASE_T0();
     const int d = A.d;
@@ -65,6 +109,8 @@ struct BfgsWarp {
     for (int c = 0; c < (DR > 0 ? 1 : kMaxC); ++c) a_col[c] = b_col[c] = 0.0;
 
     for (int j = lane; j < d; j += 32) x[j] = A.x0[(int64_t)j * A.ldx + s];
+    for (int i = d + lane; i < DR; i += 32)  // zero padding rows of row4
+      row4[4 * i] = row4[4 * i + 1] = row4[4 * i + 2] = row4[4 * i + 3] = 0.0;
     if constexpr (DR > 0) {
 #pragma unroll
       for (int i = 0; i < DR; ++i) hreg[i] = (i == lane) ? 1.0 : 0.0;
@@ -120,6 +166,13 @@ struct BfgsWarp {
       if (k >= A.cap) {
         status = ZEUS_DIVERGED;
         break;
+      }
+      if constexpr (DR > 0) {
+        if (A.k1 > 0 && k == A.k1) {  // straggler: hand over to the CTA-team kernel
+          promote(A, s, lane, hreg, pending, a_col[0], b_col[0], f0, acc, gnorm, ddir, k,
+                  ls_trials, grads, prev_trials);
+          return;
+        }
       }
       // ---- speculative batched Armijo search (linesearch.py:60-71)
       int t_acc = -1;
@@ -185,39 +238,22 @@ struct BfgsWarp {
       // ---- fused pass over H: lazy rank-2 update, u = H dg, w = H g'
       double u_own[DR > 0 ? 1 : kMaxC], w_own[DR > 0 ? 1 : kMaxC];
       if constexpr (DR > 0) {
+        // straight-line over DR rows (row4 zero-padded past d); update by select
         double u0 = 0.0, u1 = 0.0, w0 = 0.0, w1 = 0.0;
         const double aj = a_col[0], bj = b_col[0];
-        if (pending) {
 #pragma unroll
-          for (int i = 0; i < DR; ++i) {
-            if (i < d) {
-              const double2 r0 = *reinterpret_cast<const double2*>(row4 + 4 * i);
-              const double2 r1 = *reinterpret_cast<const double2*>(row4 + 4 * i + 2);
-              const double h = fma(r1.x, aj, fma(r1.y, bj, hreg[i]));
-              hreg[i] = h;
-              if (i & 1) {
-                u1 = fma(h, r0.x, u1);
-                w1 = fma(h, r0.y, w1);
-              } else {
-                u0 = fma(h, r0.x, u0);
-                w0 = fma(h, r0.y, w0);
-              }
-            }
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < DR; ++i) {
-            if (i < d) {
-              const double2 r0 = *reinterpret_cast<const double2*>(row4 + 4 * i);
-              const double h = hreg[i];
-              if (i & 1) {
-                u1 = fma(h, r0.x, u1);
-                w1 = fma(h, r0.y, w1);
-              } else {
-                u0 = fma(h, r0.x, u0);
-                w0 = fma(h, r0.y, w0);
-              }
-            }
+        for (int i = 0; i < DR; ++i) {
+          const double2 r0 = *reinterpret_cast<const double2*>(row4 + 4 * i);
+          const double2 r1 = *reinterpret_cast<const double2*>(row4 + 4 * i + 2);
+          const double upd = fma(r1.x, aj, fma(r1.y, bj, hreg[i]));
+          const double h = pending ? upd : hreg[i];
+          hreg[i] = h;
+          if (i & 1) {
+            u1 = fma(h, r0.x, u1);
+            w1 = fma(h, r0.y, w1);
+          } else {
+            u0 = fma(h, r0.x, u0);
+            w0 = fma(h, r0.y, w0);
           }
         }
         u_own[0] = u0 + u1;
@@ -389,8 +425,8 @@ __global__ void __launch_bounds__(kBfgsWarps * 32, DR > 0 ? ZEUS_MINB : 1) bfgs_
   } else {
     W.H = nullptr;
   }
-  W.row4 = v;  // [d][4] = {dg, g', dx_prev, u_prev}; 16-B aligned (offsets even)
-  v += 4 * d;
+  W.row4 = v;  // [max(d,DR)][4] = {dg, g', dx_prev, u_prev}; 16-B aligned (offsets even)
+  v += 4 * (DR > d ? DR : d);
   W.x = v;
   v += d;
   W.xn = v;
@@ -438,7 +474,8 @@ static BfgsPlan bfgs_plan(int d, int nacc, int nterms, int iter_ls) {
   P.nalpha = kAlphaTable;
   P.ldh = d;  // lanes read consecutive columns: conflict-free for any ld
   // term buffer rows: NACC * kWarpTrialRows rows of tstride, + 32 alpha scratch
-  const size_t vec = (size_t)4 * d + 5 * (size_t)d + (size_t)nacc * P.bmax * P.tstride + 32;
+  const size_t vec = (size_t)4 * std::max(d, P.dr) + 5 * (size_t)d +
+                     (size_t)nacc * P.bmax * P.tstride + 32;
   size_t per_warp = even((int)vec);
   if (P.dr == 0) {
     const size_t with_h = per_warp + hsize(d, P.ldh);
@@ -515,6 +552,9 @@ extern "C" {
 
 #ifdef ZEUS_PHASE_TIMING
 // diagnostics only (not in include/zeus_b200.h): copy out / reset the phase cycles
+int zeus_debug_team_phase_cycles(unsigned long long* out, int reset) {
+  return zeus::team_phase_cycles(out, reset);
+}
 int zeus_debug_phase_cycles(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, zeus_phase_cycles, sizeof(unsigned long long) * 8) != cudaSuccess)
     return -2;
@@ -526,11 +566,18 @@ int zeus_debug_phase_cycles(unsigned long long* out, int reset) {
 }
 #endif
 
+static int promotion_k1() {
+  const char* v = getenv("ZEUS_K1");
+  return v ? atoi(v) : 48;
+}
+static bool promotes(int d) { return d <= 16 && promotion_k1() > 0; }
+
 size_t zeus_bfgs_workspace_bytes(int d, int64_t n) {
-  (void)n;
   if (d < 1) return kWsHeader;
+  size_t extra = 0;
+  if (promotes(d)) extra = (size_t)n * carry_stride_for(d) * sizeof(double);
   const BfgsPlan P = bfgs_plan(d, 2, d, 1024);
-  if (P.dr > 0 || P.smem_h) return kWsHeader;
+  if (P.dr > 0 || P.smem_h || bfgs_team_covers(ZEUS_OBJ_RASTRIGIN, d)) return kWsHeader + extra;
   int sms = current_sm_count();
   if (sms < 1) sms = 148;
   return kWsHeader + (size_t)global_h_blocks(sms) * kBfgsWarps * (size_t)d * d * sizeof(double);
@@ -564,12 +611,25 @@ int zeus_bfgs(int obj, int d, int64_t n, const double* x0, int64_t ldx,
   A.out = *out;
   A.work = (unsigned long long*)workspace;
   A.h_global = (double*)((char*)workspace + kWsHeader);
-  int rc = check_cuda(cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), s), "memset");
+  unsigned long long* hdr = (unsigned long long*)workspace;
+  A.promo_count = hdr + 1;
+  A.promo_taken = hdr + 2;
+  int rc = check_cuda(cudaMemsetAsync(workspace, 0, 3 * sizeof(unsigned long long), s), "memset");
   if (rc) return rc;
-  if (bfgs_team_covers(obj, d) && !getenv_flag("ZEUS_NO_TEAM"))
+  if (bfgs_team_covers(obj, d) && !getenv_flag("ZEUS_NO_TEAM")) {
     rc = launch_bfgs_team(obj, A, s);
-  else
+  } else {
+    if (promotes(d) && P->iter_bfgs > promotion_k1()) {
+      A.k1 = promotion_k1();
+      A.carry = (double*)((char*)workspace + kWsHeader);
+      A.carry_stride = carry_stride_for(d);
+    }
     rc = dispatch_objective<BfgsLaunch>(obj, A, s);
+    if (rc == ZEUS_OK && A.k1 > 0) {  // phase 2: the promoted stragglers, 8 warps each
+      A.resume = 1;
+      rc = launch_bfgs_team(obj, A, s);
+    }
+  }
   if (rc == ZEUS_ERR_ARGUMENT) return set_error(rc, "unknown objective id %d", obj);
   return rc;
 }

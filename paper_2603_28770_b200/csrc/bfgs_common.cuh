@@ -29,11 +29,25 @@ struct BfgsArgs {
   int tstride;       // term-buffer row stride (odd, >= nterms)
   int bmax;          // max trials per speculative batch
   int nalpha;        // alpha table length (block smem)
+  // straggler promotion (small d): a start still running at iteration k1 is
+  // handed from the warp kernel to the CTA-team kernel through a carry record
+  int k1;                          // 0: never promote
+  double* carry;                   // [capacity][carry_stride] state records
+  int carry_stride;                // doubles per record
+  unsigned long long* promo_count; // records written (phase 1) / taken (phase 2)
+  unsigned long long* promo_taken;
+  int resume;                      // team kernel: 1 = consume carry records
 };
+
+// Carry record layout (doubles): [0] start index, [1] k, [2] ls_trials,
+// [3] grads, [4] prev_trials, [5] f0, [6..7] acc, [8] gnorm, [9] ddir,
+// then x[d], g[d], p[d], H[d][d] (row-major, the pending rank-2 update applied).
+constexpr int kCarryHead = 10;
+__host__ __device__ inline int carry_stride_for(int d) { return kCarryHead + 3 * d + d * d; }
 
 constexpr int kBfgsWarps = 4;
 #ifndef ZEUS_TERM_UNROLL
-#define ZEUS_TERM_UNROLL 4
+#define ZEUS_TERM_UNROLL 1
 #endif
 #ifndef ZEUS_MINB
 #define ZEUS_MINB 4
@@ -175,5 +189,6 @@ __device__ __forceinline__ bool grad_needs_slow(const double* xs, int d, int lan
 // ZEUS_ERR_UNSUPPORTED when no team shape covers (obj, d).
 int launch_bfgs_team(int obj, BfgsArgs A, cudaStream_t s);
 bool bfgs_team_covers(int obj, int d);
+int team_phase_cycles(unsigned long long* out, int reset);  // -DZEUS_PHASE_TIMING only
 
 }  // namespace zeus

@@ -19,40 +19,66 @@
 
 namespace zeus {
 
+#ifdef ZEUS_PHASE_TIMING
+__device__ unsigned long long zeus_team_phase_cycles[8];
+#define TPHASE(i)                                                                      \
+  do {                                                                                 \
+    const long long _n = clock64();                                                    \
+    if (tid == 0) atomicAdd(&zeus_team_phase_cycles[i], (unsigned long long)(_n - _tp)); \
+    _tp = _n;                                                                          \
+  } while (0)
+#define TPHASE_T0() long long _tp = clock64()
+#else
+#define TPHASE(i)
+#define TPHASE_T0()
+#endif
+
 namespace {
 
-// CTA-wide sum of 8 values, identical on every thread (fixed order).
+// CTA-wide sum of 8 values, identical on every thread (fixed order).  When
+// only warp 0 holds data (`w0only`: all column owners are in warp 0) the
+// other warps skip the butterfly and the cross-warp adds.
 template <int NW>
-__device__ __forceinline__ void cta_sum8(double v[8], double* red, int lane, int warp) {
+__device__ __forceinline__ void cta_sum8(double v[8], double* red, int lane, int warp,
+                                         bool w0only) {
+  if (!w0only || warp == 0) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] += __shfl_xor_sync(kFull, v[q], o);
-  }
-  if (lane == 0) {
+      for (int q = 0; q < 8; ++q) v[q] += __shfl_xor_sync(kFull, v[q], o);
+    }
+    if (lane == 0) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) red[warp * 8 + q] = v[q];
+      for (int q = 0; q < 8; ++q) red[warp * 8 + q] = v[q];
+    }
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     double s = red[q];
+    if (!w0only) {
 #pragma unroll
-    for (int w = 1; w < NW; ++w) s += red[w * 8 + q];
+      for (int w = 1; w < NW; ++w) s += red[w * 8 + q];
+    }
     v[q] = s;
   }
   __syncthreads();
 }
 
 template <int NW>
-__device__ __forceinline__ double cta_sum1(double v, double* red, int lane, int warp) {
+__device__ __forceinline__ double cta_sum1(double v, double* red, int lane, int warp,
+                                           bool w0only) {
+  if (!w0only || warp == 0) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  if (lane == 0) red[warp] = v;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (lane == 0) red[warp] = v;
+  }
   __syncthreads();
   double s = red[0];
+  if (!w0only) {
 #pragma unroll
-  for (int w = 1; w < NW; ++w) s += red[w];
+    for (int w = 1; w < NW; ++w) s += red[w];
+  }
   __syncthreads();
   return s;
 }
@@ -120,7 +146,10 @@ struct BfgsTeam {
     }
   }
 
-  __device__ void run(const BfgsArgs& A, long long s, int tid) {
+  // Fresh start s (rec == nullptr) or resume from a carry record written by
+  // the warp kernel at iteration k1 (rec != nullptr; s is read from it).
+  __device__ void run(const BfgsArgs& A, long long s, int tid, const double* rec) {
+    TPHASE_T0();
     const int d = A.d;
     const int lane = tid & 31, warp = tid >> 5;
     // column role
@@ -135,20 +164,52 @@ struct BfgsTeam {
     const bool has_col = col < d;
     const bool primary = has_col && split == 0;
     const int row0 = split * R;
+    const bool w0only = S == 1 && d <= 32;
 
     double h[R];
+    double aj = 0.0, bj = 0.0;  // pending rank-2 coefficients of my column
+    for (int i = d + tid; i < R * S; i += NT) {  // zero padding rows of row4
+      sm.row4[4 * i] = sm.row4[4 * i + 1] = sm.row4[4 * i + 2] = sm.row4[4 * i + 3] = 0.0;
+    }
+    double *x = sm.x, *xn = sm.xn, *g = sm.g, *gn = sm.gn;
+    const int nt = Obj::nterms(d);
+    double acc[Obj::NACC];
+    double f0;
+    int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
+    double gnorm = __longlong_as_double(0x7ff0000000000000LL);
+    double ddir = 0.0;
+    bool pending = false;
+
+    if (rec) {  // ---- resume (carry layout in bfgs_common.cuh)
+      k = (int)rec[1];
+      ls_trials = (int)rec[2];
+      grads = (int)rec[3];
+      prev_trials = (int)rec[4];
+      f0 = rec[5];
+#pragma unroll
+      for (int a = 0; a < Obj::NACC; ++a) acc[a] = rec[6 + a];
+      gnorm = rec[8];
+      ddir = rec[9];
+      if (primary) {
+        x[col] = rec[kCarryHead + col];
+        g[col] = rec[kCarryHead + d + col];
+        sm.p[col] = rec[kCarryHead + 2 * d + col];
+      }
+      const double* Hr = rec + kCarryHead + 3 * d;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = row0 + r;
+        h[r] = (has_col && i < d) ? Hr[(int64_t)i * d + col] : 0.0;
+      }
+      __syncthreads();
+      goto iterate;
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) h[r] = (row0 + r == col) ? 1.0 : 0.0;
-    double aj = 0.0, bj = 0.0;  // pending rank-2 coefficients of my column
-
-    double *x = sm.x, *xn = sm.xn, *g = sm.g, *gn = sm.gn;
     if (primary) x[col] = A.x0[(int64_t)col * A.ldx + s];
     __syncthreads();
 
     // f(x0)
-    const int nt = Obj::nterms(d);
-    double acc[Obj::NACC];
-    double f0;
     {
       bool oor = false;
       if (nt > 0) term_pass<Obj, FastMath, NT>(0, nt, nt, nullptr, d, x, sm.p, sm.T, A.tstride,
@@ -162,11 +223,6 @@ struct BfgsTeam {
 #pragma unroll
       for (int a = 0; a < Obj::NACC; ++a) acc[a] = sm.accv[a];
     }
-
-    int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
-    double gnorm = __longlong_as_double(0x7ff0000000000000LL);
-    double ddir = 0.0;
-    bool pending = false;
 
     if (A.stop_flag && __syncthreads_or(tid == 0 && *(volatile int*)A.stop_flag)) {
       status = ZEUS_STOPPED;
@@ -187,11 +243,15 @@ struct BfgsTeam {
         status = ZEUS_DOMAIN_ERROR;
         goto done;
       }
-      const double gg = cta_sum1<NW>(part, sm.red, lane, warp);
+      const double gg = cta_sum1<NW>(part, sm.red, lane, warp, w0only);
       gnorm = sqrt(gg);
       ddir = -gg;
     }
 
+  iterate:
+#ifdef ZEUS_PHASE_TIMING
+    _tp = clock64();
+#endif
     for (;;) {
       if (gnorm < A.theta) {
         status = ZEUS_CONVERGED;
@@ -244,6 +304,7 @@ struct BfgsTeam {
           __syncthreads();  // atab / pass_mask reuse
         }
       }
+      TPHASE(0);
       ls_trials += t_acc + 1;
       prev_trials = t_acc + 1;
       if (primary) xn[col] = x[col] + alpha * sm.p[col];
@@ -266,28 +327,27 @@ struct BfgsTeam {
         }
       }
 
+      TPHASE(1);
       // ---- fused register pass over my column: lazy update, u = H dg, w = H g'
       double u = 0.0, w = 0.0;
-      if (has_col) {
+      {
+        // straight-line over R rows: row4 is zero-padded beyond d, so rows past
+        // d contribute nothing and need no guard; the lazy update is a select
         double u0 = 0.0, u1 = 0.0, w0 = 0.0, w1 = 0.0;
+        const double* rp = sm.row4 + 4 * row0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int i = row0 + r;
-          if (i < d) {
-            const double2 ra = *reinterpret_cast<const double2*>(sm.row4 + 4 * i);
-            double hv = h[r];
-            if (pending) {
-              const double2 rb = *reinterpret_cast<const double2*>(sm.row4 + 4 * i + 2);
-              hv = fma(rb.x, aj, fma(rb.y, bj, hv));
-              h[r] = hv;
-            }
-            if (r & 1) {
-              u1 = fma(hv, ra.x, u1);
-              w1 = fma(hv, ra.y, w1);
-            } else {
-              u0 = fma(hv, ra.x, u0);
-              w0 = fma(hv, ra.y, w0);
-            }
+          const double2 ra = *reinterpret_cast<const double2*>(rp + 4 * r);
+          const double2 rb = *reinterpret_cast<const double2*>(rp + 4 * r + 2);
+          const double upd = fma(rb.x, aj, fma(rb.y, bj, h[r]));
+          const double hv = pending ? upd : h[r];
+          h[r] = hv;
+          if (r & 1) {
+            u1 = fma(hv, ra.x, u1);
+            w1 = fma(hv, ra.y, w1);
+          } else {
+            u0 = fma(hv, ra.x, u0);
+            w0 = fma(hv, ra.y, w0);
           }
         }
         u = u0 + u1;
@@ -298,6 +358,7 @@ struct BfgsTeam {
         w += __shfl_xor_sync(kFull, w, 16);
       }
 
+      TPHASE(2);
       // ---- one CTA reduction of the 8 iteration scalars
       double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       double dxj = 0.0;
@@ -313,7 +374,7 @@ struct BfgsTeam {
         part[6] = dxj * gj;
         part[7] = w * gj;
       }
-      cta_sum8<NW>(part, sm.red, lane, warp);  // ends with __syncthreads: row4 consumed
+      cta_sum8<NW>(part, sm.red, lane, warp, w0only);  // ends with __syncthreads: row4 consumed
       const double curv = part[1];
       const double ndx = sqrt(part[2]), ndg = sqrt(part[3]);
       pending = !(curv <= kCurvatureFloor * ndx * ndg);  // bfgs.py:69-71
@@ -349,7 +410,9 @@ struct BfgsTeam {
 #pragma unroll
       for (int a = 0; a < Obj::NACC; ++a) acc[a] = acc_new[a];
       gnorm = sqrt(part[0]);
-      ddir = cta_sum1<NW>(pd, sm.red, lane, warp);  // syncs: p / row4 visible
+      TPHASE(3);
+      ddir = cta_sum1<NW>(pd, sm.red, lane, warp, w0only);  // syncs: p / row4 visible
+      TPHASE(4);
       ++k;
       if (A.stop_flag && __syncthreads_or(tid == 0 && *(volatile int*)A.stop_flag)) {
         status = ZEUS_STOPPED;
@@ -385,8 +448,8 @@ __global__ void __launch_bounds__(NW * 32, 1) bfgs_team_kernel(BfgsArgs A) {
   double* v = smem;
   sm.alpha_tab = v;
   v += A.nalpha;
-  sm.row4 = v;  // 16-B aligned: nalpha is even
-  v += 4 * d;
+  sm.row4 = v;  // 16-B aligned: nalpha is even; R*S rows (zero padding past d)
+  v += 4 * R * S;
   sm.x = v;
   v += d;
   sm.xn = v;
@@ -417,13 +480,20 @@ __global__ void __launch_bounds__(NW * 32, 1) bfgs_team_kernel(BfgsArgs A) {
     }
   }
   BfgsTeam<Obj, NW, R, S> T{sm};
+  const long long nwork = A.resume ? (long long)*A.promo_count : A.n;
   for (;;) {
-    if (tid == 0) *sm.start = (long long)atomicAdd(A.work, 1ull);
+    if (tid == 0)
+      *sm.start = (long long)atomicAdd(A.resume ? A.promo_taken : A.work, 1ull);
     __syncthreads();
-    const long long s = *sm.start;
+    const long long w = *sm.start;
     __syncthreads();
-    if (s >= A.n) break;
-    T.run(A, s, tid);
+    if (w >= nwork) break;
+    if (A.resume) {
+      const double* rec = A.carry + (size_t)w * A.carry_stride;
+      T.run(A, (long long)rec[0], tid, rec);
+    } else {
+      T.run(A, w, tid, nullptr);
+    }
   }
 }
 
@@ -431,9 +501,9 @@ namespace {
 
 constexpr int kTeamTermCap = 1024;
 
-size_t team_smem_bytes(int d, int nacc, int nw, int bmax, int tstride, int nalpha) {
-  return sizeof(double) *
-         ((size_t)nalpha + 9 * (size_t)d + (size_t)nacc * bmax * tstride + 32 + 32 + 64 + 8 * nw + 2);
+size_t team_smem_bytes(int d, int rows, int nacc, int nw, int bmax, int tstride, int nalpha) {
+  return sizeof(double) * ((size_t)nalpha + 4 * (size_t)rows + 5 * (size_t)d +
+                           (size_t)nacc * bmax * tstride + 32 + 32 + 64 + 8 * nw + 2);
 }
 
 template <class Obj, int NW, int R, int S>
@@ -442,7 +512,7 @@ int launch_shape(BfgsArgs A, cudaStream_t s) {
   A.tstride = nt | 1;
   A.bmax = std::max(1, std::min(32, kTeamTermCap / nt));
   A.nalpha = kAlphaTable;
-  const size_t smem = team_smem_bytes(A.d, Obj::NACC, NW, A.bmax, A.tstride, A.nalpha);
+  const size_t smem = team_smem_bytes(A.d, R * S, Obj::NACC, NW, A.bmax, A.tstride, A.nalpha);
   auto kern = bfgs_team_kernel<Obj, NW, R, S>;
   int rc = check_cuda(
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
@@ -455,7 +525,7 @@ int launch_shape(BfgsArgs A, cudaStream_t s) {
   const int sms = current_sm_count();
   if (per_sm < 1 || sms < 1) return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs team: does not fit");
   int64_t grid = (int64_t)per_sm * sms;
-  if (grid > A.n) grid = A.n;
+  if (!A.resume && grid > A.n) grid = A.n;
   kern<<<(unsigned)grid, NW * 32, smem, s>>>(A);
   return check_launch("bfgs_team_kernel");
 }
@@ -464,6 +534,10 @@ struct TeamLaunch {
   template <class Obj>
   static int run(BfgsArgs A, cudaStream_t s) {
     const int d = A.d;
+    if (A.resume) {  // stragglers of the warp kernel (d <= 16): 8 warps per start
+      if (d <= 16) return launch_shape<Obj, 8, 16, 1>(A, s);
+      return set_error(ZEUS_ERR_UNSUPPORTED, "team resume: d=%d > 16", d);
+    }
     if constexpr (Obj::kId == ZEUS_OBJ_GOLDSTEIN_PRICE) {
       return set_error(ZEUS_ERR_UNSUPPORTED, "team: goldstein_price is 2-D");
     } else {
@@ -478,6 +552,18 @@ struct TeamLaunch {
 };
 
 }  // namespace
+
+#ifdef ZEUS_PHASE_TIMING
+int team_phase_cycles(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, zeus_team_phase_cycles, 8 * sizeof(unsigned long long)) != cudaSuccess)
+    return -2;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(zeus_team_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 bool bfgs_team_covers(int obj, int d) {
   return obj != ZEUS_OBJ_GOLDSTEIN_PRICE && d > 32 && d <= 128;

@@ -18,6 +18,7 @@ Buffers (HBM, SoA, float64):
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -93,7 +94,9 @@ def run_bfgs(obj: int, x0: torch.Tensor, params: _capi.BfgsParams, out: BfgsBuff
     _capi.check(L.zeus_bfgs(obj, d, n, x0.data_ptr(), x0.stride(0), params, int(required_c),
                             counter, flag, out.c_struct(n), ws.data_ptr(),
                             _device.stream_ptr(device)), "bfgs")
-    LAUNCHES[0] += 1
+    # small d: warp kernel + the CTA-team kernel for promoted stragglers
+    k1 = int(os.environ.get("ZEUS_K1", "48"))
+    LAUNCHES[0] += 2 if (d <= 16 and k1 > 0 and params.iter_bfgs > k1) else 1
 
 
 class SwarmShard:

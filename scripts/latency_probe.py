@@ -32,7 +32,7 @@ timing = hasattr(L, "zeus_debug_phase_cycles")
 buf = (ctypes.c_ulonglong * 8)()
 for rep in range(3):
     if timing:
-        torch.cuda.synchronize(); L.zeus_debug_phase_cycles(buf, 1)
+        torch.cuda.synchronize(); L.zeus_debug_phase_cycles(buf, 1); L.zeus_debug_team_phase_cycles(buf, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); engine.run_bfgs(z.objective_id(spec.fn), x0, P, out, dev); e1.record(); e1.synchronize()
     ms = e0.elapsed_time(e1)
@@ -40,6 +40,9 @@ k = int(out.iterations[0].item())
 if timing:
     L.zeus_debug_phase_cycles(buf, 0)
     names = ["line search", "gradient", "H pass", "8-value reduction+p'", "ddir+swap", "prologue"]
-    print("phase cycles per iteration:", {n: round(buf[i] / max(k, 1)) for i, n in enumerate(names)})
+    print("warp phase cycles per iteration:", {n: round(buf[i] / max(k, 1)) for i, n in enumerate(names)})
+    L.zeus_debug_team_phase_cycles(buf, 0)
+    tn = ["line search", "gradient", "H pass", "8-value reduction+p'", "ddir"]
+    print("team phase cycles total (per iteration of k):", {n: round(buf[i] / max(k, 1)) for i, n in enumerate(tn)})
 print(json.dumps({"objective": obj, "d": d, "straggler_iterations": k, "ms": ms, "us_per_iteration": ms * 1e3 / max(k, 1),
                   "cycles_per_iteration_at_1965MHz": ms * 1e-3 * 1.965e9 / max(k, 1)}))

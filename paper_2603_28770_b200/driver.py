@@ -317,10 +317,8 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
         best_dev[0] = math.nan
         best_dev[1] = -1.0
     if world > 1:
-        cands = torch.empty(world * 2, dtype=torch.float64, device=dev)
-        torch.distributed.all_gather_into_tensor(cands, best_dev, group=process_group)
+        best_dev = engine.gather_candidates(best_dev, process_group)  # resolved on the host
         torch.distributed.all_reduce(tallies, group=process_group)
-        best_dev = cands  # resolved on the host below (world pairs)
     ev_end.record(stream)
 
     # ---- results to host (part of the end-to-end wall time)
@@ -358,13 +356,10 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
             raise NoValidOptimumError("all runs ended in domain errors")
         bidx = int(np.flatnonzero(valid)[np.argmin(f_h[:m][valid])])
     else:
-        pairs = best_host.reshape(-1, 2)
-        ok = pairs[:, 1] >= 0
-        if not ok.any():
+        gidx = engine.resolve_minloc(best_host.reshape(-1, 2).tolist())
+        if gidx < 0:
             raise NoValidOptimumError("all runs ended in domain errors")
-        cand = pairs[ok]
-        order = np.lexsort((cand[:, 1], cand[:, 0]))
-        bidx = int(cand[order[0], 1]) - base
+        bidx = gidx - base
     per_run = OutcomeList(x_host, f_h, gn_h, it_h, st_h, length=m)
     if not 0 <= bidx < m:
         # best lives on another rank and per_run is local (gather=False)

@@ -155,6 +155,41 @@ def local_barrier(shard: SwarmShard) -> None:
     shard.select(shard.cand, 1)
 
 
+def gather_candidates(cand: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather each shard's candidate vector (any device / backend):
+    returns [world * len(cand)] in rank order."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    gathered = torch.empty(world * cand.numel(), dtype=cand.dtype, device=cand.device)
+    dist.all_gather_into_tensor(gathered, cand.contiguous(), group=group)
+    return gathered
+
+
+def resolve_minloc(pairs) -> int:
+    """np.argmin order over gathered (f, global_idx) pairs, idx < 0 = empty
+    shard: the first NaN wins, else the smallest f, ties to the lowest index.
+    Returns the winning global index or -1.  (Host mirror of the device rule
+    in csrc/zeus_common.cuh argmin_better, used for the final `best`.)"""
+    import math
+
+    best_f, best_i = 0.0, -1
+    for f, i in pairs:
+        i = int(i)
+        if i < 0:
+            continue
+        if best_i < 0:
+            best_f, best_i = f, i
+            continue
+        fn, bn = math.isnan(f), math.isnan(best_f)
+        if fn or bn:
+            if (fn and bn and i < best_i) or (fn and not bn):
+                best_f, best_i = f, i
+        elif f < best_f or (f == best_f and i < best_i):
+            best_f, best_i = f, i
+    return best_i
+
+
 def make_dist_barrier(group=None) -> Barrier:
     """Multi-GPU barrier: all-gather every shard's [f, idx, x] candidate over
     NCCL (one collective per sweep) and select the np.argmin winner on device."""
@@ -163,8 +198,6 @@ def make_dist_barrier(group=None) -> Barrier:
     world = dist.get_world_size(group)
 
     def barrier(shard: SwarmShard) -> None:
-        gathered = torch.empty(world * (shard.d + 2), dtype=torch.float64, device=shard.device)
-        dist.all_gather_into_tensor(gathered, shard.cand, group=group)
-        shard.select(gathered, world)
+        shard.select(gather_candidates(shard.cand, group), world)
 
     return barrier

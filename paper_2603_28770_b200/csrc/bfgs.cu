@@ -121,7 +121,8 @@ struct BfgsWarp {
     __syncwarp();
 
     double acc[Obj::NACC];
-    double f0 = eval_batch<Obj>(0, nullptr, d, x, p, T, A.tstride, A.bmax, lane, acc);
+    double* TT = T + Obj::NACC * A.bmax * A.tstride;  // term tangents [KT][bmax][tstride]
+    double f0 = eval_batch<Obj>(0, nullptr, d, x, p, T, TT, A.tstride, A.bmax, lane, acc);
     f0 = __shfl_sync(kFull, f0, 0);
 #pragma unroll
     for (int a = 0; a < Obj::NACC; ++a) acc[a] = __shfl_sync(kFull, acc[a], 0);
@@ -140,9 +141,9 @@ struct BfgsWarp {
       ++grads;
       bool err = false;
       double part = 0.0;
-      const bool slow = grad_needs_slow<Obj>(x, d, lane);
+      const TanRow tan0{TT, A.bmax, A.tstride, 0};
       for (int j = lane; j < d; j += 32) {
-        const double gj = grad_at<Obj>(x, j, d, acc, err, slow);
+        const double gj = Obj::grad_from_tan(tan0, j, d, acc, err);
         g[j] = gj;
         p[j] = -gj;  // H0 = I: -(I @ g) is exact
         part = fma(gj, gj, part);
@@ -177,16 +178,18 @@ struct BfgsWarp {
       // ---- speculative batched Armijo search (linesearch.py:60-71)
       int t_acc = -1;
       double f_new = 0.0, acc_new[Obj::NACC];
+      int src_row = 0;  // batch row of the accepted trial (its tangents in TT)
       {
         int t0 = 0;
         int B = min(max(prev_trials, max(1, 32 / max(Obj::nterms(d), 1))), A.bmax);
         for (;;) {
           B = min(B, A.iter_ls + 1 - t0);
-          double* atab = T + Obj::NACC * A.bmax * A.tstride;  // per-warp alpha scratch
+          double* atab = TT + Obj::KT * A.bmax * A.tstride;  // per-warp alpha scratch
           if (lane < B) atab[lane] = alpha_at(A, t0 + lane);
           __syncwarp();
           double accb[Obj::NACC];
-          const double fb = eval_batch<Obj>(B, atab, d, x, p, T, A.tstride, A.bmax, lane, accb);
+          const double fb =
+              eval_batch<Obj>(B, atab, d, x, p, T, TT, A.tstride, A.bmax, lane, accb);
           bool pass = false;
           if (lane < B) pass = fb <= f0 + A.c1 * atab[lane] * ddir;  // NaN fails
           const unsigned m = __ballot_sync(kFull, pass);
@@ -198,6 +201,7 @@ struct BfgsWarp {
           }
           if (src >= 0) {
             t_acc = t0 + src;
+            src_row = src;
             f_new = __shfl_sync(kFull, fb, src);
 #pragma unroll
             for (int a = 0; a < Obj::NACC; ++a) acc_new[a] = __shfl_sync(kFull, accb[a], src);
@@ -219,9 +223,9 @@ struct BfgsWarp {
       double part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       {
         bool err = false;
-        const bool slow = grad_needs_slow<Obj>(xn, d, lane);
+        const TanRow tanr{TT, A.bmax, A.tstride, src_row};
         for (int j = lane; j < d; j += 32) {
-          const double gj = grad_at<Obj>(xn, j, d, acc_new, err, slow);
+          const double gj = Obj::grad_from_tan(tanr, j, d, acc_new, err);
           const double dgj = gj - g[j];
           gn[j] = gj;
           row4[4 * j + 0] = dgj;
@@ -475,7 +479,7 @@ static BfgsPlan bfgs_plan(int d, int nacc, int nterms, int iter_ls) {
   P.ldh = d;  // lanes read consecutive columns: conflict-free for any ld
   // term buffer rows: NACC * kWarpTrialRows rows of tstride, + 32 alpha scratch
   const size_t vec = (size_t)4 * std::max(d, P.dr) + 5 * (size_t)d +
-                     (size_t)nacc * P.bmax * P.tstride + 32;
+                     (size_t)(nacc + 2) * P.bmax * P.tstride + 32;  // + KT <= 2 tangent rows
   size_t per_warp = even((int)vec);
   if (P.dr == 0) {
     const size_t with_h = per_warp + hsize(d, P.ldh);

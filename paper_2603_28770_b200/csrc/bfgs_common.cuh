@@ -102,11 +102,12 @@ __device__ __forceinline__ void warp_sum8(double v[8]) {
 template <class Obj, class M, int NTH = 32>
 __device__ __forceinline__ void term_pass(int B, int nt, int total, const double* alpha_of,
                                           int d, const double* x, const double* p, double* T,
-                                          int tstride, int rows, int lane, bool& oor) {
+                                          double* TT, int tstride, int rows, int lane,
+                                          bool& oor) {
   const int step_b = NTH / nt, step_j = NTH - step_b * nt;
   int b = lane / nt, j = lane - b * nt;
   for (int q0 = lane; q0 < total; q0 += NTH * kU) {
-    double t[kU][Obj::NACC];
+    double t[kU][Obj::NACC], tn[kU][Obj::KT];
     int bb[kU], jj[kU];
 #pragma unroll
     for (int r = 0; r < kU; ++r) {
@@ -114,9 +115,9 @@ __device__ __forceinline__ void term_pass(int B, int nt, int total, const double
       jj[r] = j;
       if (q0 + NTH * r < total) {
         if (B > 0) {
-          Obj::template term<M>(TrialX{x, p, alpha_of[b]}, j, d, t[r], oor);
+          Obj::template term_tan<M>(TrialX{x, p, alpha_of[b]}, j, d, t[r], tn[r], oor);
         } else {
-          Obj::template term<M>(DenseX{x}, j, d, t[r], oor);
+          Obj::template term_tan<M>(DenseX{x}, j, d, t[r], tn[r], oor);
         }
       }
       j += step_j;
@@ -131,26 +132,30 @@ __device__ __forceinline__ void term_pass(int B, int nt, int total, const double
       if (q0 + NTH * r < total) {
 #pragma unroll
         for (int a = 0; a < Obj::NACC; ++a) T[(a * rows + bb[r]) * tstride + jj[r]] = t[r][a];
+#pragma unroll
+        for (int k = 0; k < Obj::KT; ++k) TT[(k * rows + bb[r]) * tstride + jj[r]] = tn[r][k];
       }
     }
   }
 }
 
-// Evaluate B trial points x + alpha_of[b] p; lane b < B returns trial b's
-// value and accumulators (reference-order fold).  B == 0 evaluates x itself.
+// Evaluate B trial points x + alpha_of[b] p (values AND term tangents);
+// lane b < B returns trial b's value and accumulators (reference-order fold).
+// B == 0 evaluates x itself.
 template <class Obj>
 __device__ __forceinline__ double eval_batch(int B, const double* alpha_of, int d,
                                              const double* x, const double* p, double* T,
-                                             int tstride, int rows, int lane,
+                                             double* TT, int tstride, int rows, int lane,
                                              double acc[Obj::NACC]) {
   const int nt = Obj::nterms(d);
   const int nb = B > 0 ? B : 1;
   const int total = nb * nt;
   if (total > 0) {
     bool oor = false;
-    term_pass<Obj, FastMath>(B, nt, total, alpha_of, d, x, p, T, tstride, rows, lane, oor);
+    term_pass<Obj, FastMath>(B, nt, total, alpha_of, d, x, p, T, TT, tstride, rows, lane, oor);
     if (__any_sync(kFull, oor))  // some |2 pi x| > kTrigMax: redo with CUDA libm
-      term_pass<Obj, PreciseMath>(B, nt, total, alpha_of, d, x, p, T, tstride, rows, lane, oor);
+      term_pass<Obj, PreciseMath>(B, nt, total, alpha_of, d, x, p, T, TT, tstride, rows, lane,
+                                  oor);
   }
   __syncwarp();
   double f = 0.0;

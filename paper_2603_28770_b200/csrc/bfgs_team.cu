@@ -87,7 +87,7 @@ __device__ __forceinline__ double cta_sum1(double v, double* red, int lane, int 
 
 // Shared-memory layout of one CTA (one start), in doubles.
 struct TeamSmem {
-  double *alpha_tab, *x, *xn, *p, *g, *gn, *row4, *T, *atab, *fval, *accv, *red;
+  double *alpha_tab, *x, *xn, *p, *g, *gn, *row4, *T, *TT, *atab, *fval, *accv, *red;
   unsigned* pass_mask;
   long long* start;
 };
@@ -212,11 +212,11 @@ struct BfgsTeam {
     // f(x0)
     {
       bool oor = false;
-      if (nt > 0) term_pass<Obj, FastMath, NT>(0, nt, nt, nullptr, d, x, sm.p, sm.T, A.tstride,
-                                                A.bmax, tid, oor);
+      if (nt > 0) term_pass<Obj, FastMath, NT>(0, nt, nt, nullptr, d, x, sm.p, sm.T, sm.TT,
+                                                A.tstride, A.bmax, tid, oor);
       if (__syncthreads_or(oor))
-        term_pass<Obj, PreciseMath, NT>(0, nt, nt, nullptr, d, x, sm.p, sm.T, A.tstride,
-                                        A.bmax, tid, oor);
+        term_pass<Obj, PreciseMath, NT>(0, nt, nt, nullptr, d, x, sm.p, sm.T, sm.TT,
+                                        A.tstride, A.bmax, tid, oor);
       fold(A, 1, d, tid, lane, warp);
       __syncthreads();
       f0 = sm.fval[0];
@@ -231,10 +231,9 @@ struct BfgsTeam {
     {  // first gradient; p = -g (H0 = I)
       ++grads;
       bool err = false;
-      const bool slow = __syncthreads_or(primary && !trig_in_range(kTwoPi * x[col]));
       double part = 0.0;
       if (primary) {
-        const double gj = grad_at<Obj>(x, col, d, acc, err, slow);
+        const double gj = Obj::grad_from_tan(TanRow{sm.TT, A.bmax, A.tstride, 0}, col, d, acc, err);
         g[col] = gj;
         sm.p[col] = -gj;
         part = gj * gj;
@@ -262,7 +261,7 @@ struct BfgsTeam {
         break;
       }
       // ---- speculative batched Armijo search (linesearch.py:60-71)
-      int t_acc;
+      int t_acc, src_row = 0;
       double f_new, acc_new[Obj::NACC], alpha;
       {
         int t0 = 0;
@@ -275,10 +274,10 @@ struct BfgsTeam {
           const int total = B * nt;
           bool oor = false;
           if (total > 0)
-            term_pass<Obj, FastMath, NT>(B, nt, total, sm.atab, d, x, sm.p, sm.T, A.tstride,
-                                         A.bmax, tid, oor);
+            term_pass<Obj, FastMath, NT>(B, nt, total, sm.atab, d, x, sm.p, sm.T, sm.TT,
+                                         A.tstride, A.bmax, tid, oor);
           if (__syncthreads_or(oor))
-            term_pass<Obj, PreciseMath, NT>(B, nt, total, sm.atab, d, x, sm.p, sm.T,
+            term_pass<Obj, PreciseMath, NT>(B, nt, total, sm.atab, d, x, sm.p, sm.T, sm.TT,
                                             A.tstride, A.bmax, tid, oor);
           fold(A, B, d, tid, lane, warp);
           __syncthreads();
@@ -293,6 +292,7 @@ struct BfgsTeam {
           else if (t0 + B > A.iter_ls) src = B - 1;  // fell through: last trial
           if (src >= 0) {
             t_acc = t0 + src;
+            src_row = src;
             f_new = sm.fval[src];
 #pragma unroll
             for (int a = 0; a < Obj::NACC; ++a) acc_new[a] = sm.accv[src * 2 + a];
@@ -307,16 +307,15 @@ struct BfgsTeam {
       TPHASE(0);
       ls_trials += t_acc + 1;
       prev_trials = t_acc + 1;
-      if (primary) xn[col] = x[col] + alpha * sm.p[col];
-      __syncthreads();
-
-      // ---- gradient at x_new; DomainError leaves x, k unchanged
+      // ---- x_new and the gradient there, assembled from the accepted trial's
+      // term tangents (computed in the term pass); DomainError leaves x, k
       ++grads;
       {
         bool err = false;
-        const bool slow = __syncthreads_or(primary && !trig_in_range(kTwoPi * xn[col]));
         if (primary) {
-          const double gj = grad_at<Obj>(xn, col, d, acc_new, err, slow);
+          xn[col] = x[col] + alpha * sm.p[col];
+          const double gj =
+              Obj::grad_from_tan(TanRow{sm.TT, A.bmax, A.tstride, src_row}, col, d, acc_new, err);
           gn[col] = gj;
           sm.row4[4 * col + 0] = gj - g[col];
           sm.row4[4 * col + 1] = gj;
@@ -462,6 +461,8 @@ __global__ void __launch_bounds__(NW * 32, 1) bfgs_team_kernel(BfgsArgs A) {
   v += d;
   sm.T = v;
   v += Obj::NACC * A.bmax * A.tstride;
+  sm.TT = v;
+  v += Obj::KT * A.bmax * A.tstride;
   sm.atab = v;
   v += 32;
   sm.fval = v;
@@ -501,9 +502,10 @@ namespace {
 
 constexpr int kTeamTermCap = 1024;
 
-size_t team_smem_bytes(int d, int rows, int nacc, int nw, int bmax, int tstride, int nalpha) {
+size_t team_smem_bytes(int d, int rows, int nacc, int kt, int nw, int bmax, int tstride,
+                       int nalpha) {
   return sizeof(double) * ((size_t)nalpha + 4 * (size_t)rows + 5 * (size_t)d +
-                           (size_t)nacc * bmax * tstride + 32 + 32 + 64 + 8 * nw + 2);
+                           (size_t)(nacc + kt) * bmax * tstride + 32 + 32 + 64 + 8 * nw + 2);
 }
 
 template <class Obj, int NW, int R, int S>
@@ -512,7 +514,8 @@ int launch_shape(BfgsArgs A, cudaStream_t s) {
   A.tstride = nt | 1;
   A.bmax = std::max(1, std::min(32, kTeamTermCap / nt));
   A.nalpha = kAlphaTable;
-  const size_t smem = team_smem_bytes(A.d, R * S, Obj::NACC, NW, A.bmax, A.tstride, A.nalpha);
+  const size_t smem =
+      team_smem_bytes(A.d, R * S, Obj::NACC, Obj::KT, NW, A.bmax, A.tstride, A.nalpha);
   auto kern = bfgs_team_kernel<Obj, NW, R, S>;
   int rc = check_cuda(
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),

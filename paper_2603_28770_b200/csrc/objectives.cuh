@@ -107,6 +107,13 @@ __device__ __forceinline__ double tangent<Dual>(const Dual& v) { return v.d; }
 //   term<M>(X, j, d, t[NACC], oor)   term j (X(j) -> coordinate j), math policy M
 //   finish(acc[NACC], d, err)
 //   grad<M>(X, i, d, acc, err, oor)  d f / d x_i from the Dual rules (see header)
+//   KT, term_tan<M>(X, j, d, t[NACC], tan[KT], oor)
+//                             term j's value AND its tangents w.r.t. the
+//                             coordinates it contains (one Dual pass per
+//                             coordinate; sin comes free with the cos)
+//   grad_from_tan(TA, i, d, acc, err)  d f / d x_i assembled from the stored
+//                             term tangents TA(j, k) -- the fold of the
+//                             non-zero tangents in the reference's order
 // ---------------------------------------------------------------------------
 
 // objectives.py:33-45  (total = total + (a*a + 100*(b*b)), a = 1-x_i, b = x_{i+1}-x_i^2)
@@ -126,6 +133,30 @@ struct Rosenbrock {
     t[0] = term2<double>(x(j), x(j + 1));
   }
   __device__ static double finish(const double acc[1], int, bool&) { return acc[0]; }
+  static constexpr int KT = 2;  // d term_j / d x_j, d term_j / d x_{j+1}
+  template <class M, class X>
+  __device__ static void term_tan(const X& x, int j, int, double t[1], double tan[2], bool&) {
+    const double xj = x(j), xj1 = x(j + 1);
+    const Dual e0 = term2<Dual>(Dual{xj, 1.0}, Dual{xj1, 0.0});
+    const Dual e1 = term2<Dual>(Dual{xj, 0.0}, Dual{xj1, 1.0});
+    t[0] = e0.r;
+    tan[0] = e0.d;
+    tan[1] = e1.d;
+  }
+  template <class TA>
+  __device__ static double grad_from_tan(const TA& tan, int i, int d, const double*, bool&) {
+    double g = 0.0;
+    bool any = false;
+    if (i >= 1) {
+      g = tan(i - 1, 1);
+      any = true;
+    }
+    if (i + 1 < d) {
+      const double t = tan(i, 0);
+      g = any ? g + t : t;
+    }
+    return g;
+  }
   template <class M = AutoMath, class X>
   __device__ static double grad(const X& x, int i, int d, const double*, bool&, bool&) {
     // seed x_i: term i-1 sees it as x_{j+1}, term i as x_j
@@ -163,6 +194,18 @@ struct Rastrigin {
   __device__ static double grad(const X& x, int i, int, const double*, bool&, bool& oor) {
     return term1<M, Dual>(Dual{x(i), 1.0}, oor).d;
   }
+  static constexpr int KT = 1;
+  template <class M, class X>
+  __device__ static void term_tan(const X& x, int j, int, double t[1], double tan[1],
+                                  bool& oor) {
+    const Dual e = term1<M, Dual>(Dual{x(j), 1.0}, oor);
+    t[0] = e.r;
+    tan[0] = e.d;
+  }
+  template <class TA>
+  __device__ static double grad_from_tan(const TA& tan, int i, int, const double*, bool&) {
+    return tan(i, 0);
+  }
 };
 
 // objectives.py:64-85
@@ -196,6 +239,22 @@ struct Ackley {
     // real parts: the full sequential sums; tangents: the only non-zero term
     return outer<Dual>(Dual{acc[0], sq.d}, Dual{acc[1], cs.d}, d, err).d;
   }
+  static constexpr int KT = 2;  // d(x_j^2)/dx_j, d cos(2 pi x_j)/dx_j
+  template <class M, class X>
+  __device__ static void term_tan(const X& x, int j, int, double t[2], double tan[2],
+                                  bool& oor) {
+    Dual sq, cs;
+    terms<M, Dual>(Dual{x(j), 1.0}, sq, cs, oor);
+    t[0] = sq.r;
+    t[1] = cs.r;
+    tan[0] = sq.d;
+    tan[1] = cs.d;
+  }
+  template <class TA>
+  __device__ static double grad_from_tan(const TA& tan, int i, int d, const double* acc,
+                                         bool& err) {
+    return outer<Dual>(Dual{acc[0], tan(i, 0)}, Dual{acc[1], tan(i, 1)}, d, err).d;
+  }
 };
 
 // objectives.py:88-113 (d == 2 only; validated on the host)
@@ -228,9 +287,30 @@ struct GoldsteinPrice {
     return i == 0 ? eval<Dual>(Dual{x(0), 1.0}, Dual{x(1), 0.0}).d
                   : eval<Dual>(Dual{x(0), 0.0}, Dual{x(1), 1.0}).d;
   }
+  static constexpr int KT = 2;  // both partials of the single term
+  template <class M, class X>
+  __device__ static void term_tan(const X& x, int, int, double t[1], double tan[2], bool&) {
+    const Dual e0 = eval<Dual>(Dual{x(0), 1.0}, Dual{x(1), 0.0});
+    const Dual e1 = eval<Dual>(Dual{x(0), 0.0}, Dual{x(1), 1.0});
+    t[0] = e0.r;
+    tan[0] = e0.d;
+    tan[1] = e1.d;
+  }
+  template <class TA>
+  __device__ static double grad_from_tan(const TA& tan, int i, int, const double*, bool&) {
+    return tan(0, i);
+  }
 };
 
 // ---- accessors ------------------------------------------------------------
+// Tangent slot k of term j for batch row b (buffer [KT][rows][tstride]).
+struct TanRow {
+  const double* T;
+  int rows, tstride, b;
+  __device__ __forceinline__ double operator()(int j, int k) const {
+    return T[(k * rows + b) * tstride + j];
+  }
+};
 struct StridedX {
   const double* p;
   long long stride;

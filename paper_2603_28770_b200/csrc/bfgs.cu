@@ -40,12 +40,83 @@
 
 namespace zeus {
 
-template <class Obj, int DR>
+// Named-barrier helpers for the helper-warp mode (warp 0 and the helpers
+// meet at barrier 1 from different code paths, which PTX bar.sync permits).
+__device__ __forceinline__ void bar1(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+__device__ __forceinline__ bool bar1_or(int n, bool v) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, 1, %2, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((int)v), "r"(n)
+      : "memory");
+  return r != 0;
+}
+
+// Task published by the driving warp to its helper warps (NH > 0).
+struct HelperTask {
+  int B;      // trials in the batch (0: evaluate x itself); -1: exit
+  int xsel;   // which smem buffer holds the current x (x / xn swap)
+};
+
+// NH == 0: one warp per start, blocks of kBfgsWarps independent warps.
+// NH  > 0: one start per CTA of 1 + NH warps; warp 0 runs the iteration and
+//          the NH helper warps only evaluate the speculative term batches
+//          (promoted stragglers: the batch work spreads over 32 (1+NH) lanes
+//          while everything else stays warp-synchronous in warp 0).
+template <class Obj, int DR, int NH = 0>
 struct BfgsWarp {
+  static constexpr int NT = 32 * (NH + 1);
   // shared-memory vectors of this warp (each d doubles unless noted)
   double *x, *xn, *p, *g, *gn, *row4, *T;
   double* H;  // smem / global H (DR == 0)
   const double* alpha_tab;
+  HelperTask* task;
+  double* xbuf[2];  // the two x buffers (helper mode needs to name them)
+
+  // Evaluate a batch: NH == 0 -> eval_batch over the warp; NH > 0 -> publish
+  // the task, all 32 (1+NH) threads run the term pass, warp 0 folds.
+  __device__ __forceinline__ double evalb(const BfgsArgs& A, int B, const double* alphas, int d,
+                                          double* TT, int lane, double acc[Obj::NACC]) {
+    if constexpr (NH == 0) {
+      return eval_batch<Obj>(B, alphas, d, x, p, T, TT, A.tstride, A.bmax, lane, acc);
+    } else {
+      if (lane == 0) {
+        task->B = B;
+        task->xsel = (x == xbuf[0]) ? 0 : 1;
+      }
+      __syncwarp();
+      bar1(NT);  // A: task, x, p, alphas visible to the helpers
+      const int nt = Obj::nterms(d);
+      const int total = (B > 0 ? B : 1) * nt;
+      bool oor = false;
+      if (total > 0)
+        term_pass<Obj, FastMath, NT>(B, nt, total, alphas, d, x, p, T, TT, A.tstride, A.bmax,
+                                     lane, oor);
+      if (bar1_or(NT, oor)) {  // B: every term written
+        if (total > 0)
+          term_pass<Obj, PreciseMath, NT>(B, nt, total, alphas, d, x, p, T, TT, A.tstride,
+                                          A.bmax, lane, oor);
+        bar1(NT);
+      }
+      const int nb = B > 0 ? B : 1;
+      double f = 0.0;
+      if (lane < nb) {
+#pragma unroll
+        for (int a = 0; a < Obj::NACC; ++a) {
+          const double* row = T + (a * A.bmax + lane) * A.tstride;
+          double sacc = Obj::init(a, d);
+          for (int j = 0; j < nt; ++j) sacc = sacc + row[j];
+          acc[a] = sacc;
+        }
+        bool err = false;
+        f = Obj::finish(acc, d, err);
+      }
+      __syncwarp();
+      return f;
+    }
+  }
 
   __device__ __forceinline__ double alpha_at(const BfgsArgs& A, int t) const {
     if (t < A.nalpha) return alpha_tab[t];
@@ -98,7 +169,9 @@ struct BfgsWarp {
     __syncwarp();
   }
 
-  __device__ void run(const BfgsArgs& A, long long s, int lane) {
+  // Fresh start s from x0, or (rec != nullptr, helper mode) resume a start
+  // promoted by the warp kernel from its carry record (bfgs_common.cuh).
+  __device__ void run(const BfgsArgs& A, long long s, int lane, const double* rec = nullptr) {
     PHASE_T0();
     const int d = A.d;
     const int C = (d + 31) >> 5;  // columns per lane
@@ -107,10 +180,41 @@ struct BfgsWarp {
     double a_col[DR > 0 ? 1 : kMaxC], b_col[DR > 0 ? 1 : kMaxC];
 #pragma unroll
     for (int c = 0; c < (DR > 0 ? 1 : kMaxC); ++c) a_col[c] = b_col[c] = 0.0;
+    double acc[Obj::NACC];
+    double* TT = T + Obj::NACC * A.bmax * A.tstride;  // term tangents [KT][bmax][tstride]
+    double f0 = 0.0;
+    int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
+    double gnorm = __longlong_as_double(0x7ff0000000000000LL);
+    double ddir = 0.0;
+    bool pending = false;
 
-    for (int j = lane; j < d; j += 32) x[j] = A.x0[(int64_t)j * A.ldx + s];
     for (int i = d + lane; i < DR; i += 32)  // zero padding rows of row4
       row4[4 * i] = row4[4 * i + 1] = row4[4 * i + 2] = row4[4 * i + 3] = 0.0;
+    if (rec) {
+      k = (int)rec[1];
+      ls_trials = (int)rec[2];
+      grads = (int)rec[3];
+      prev_trials = (int)rec[4];
+      f0 = rec[5];
+      acc[0] = rec[6];
+      if (Obj::NACC > 1) acc[Obj::NACC - 1] = rec[7];
+      gnorm = rec[8];
+      ddir = rec[9];
+      for (int j = lane; j < d; j += 32) {
+        x[j] = rec[kCarryHead + j];
+        g[j] = rec[kCarryHead + d + j];
+        p[j] = rec[kCarryHead + 2 * d + j];
+      }
+      if constexpr (DR > 0) {
+        const double* Hr = rec + kCarryHead + 3 * d;
+#pragma unroll
+        for (int i = 0; i < DR; ++i) hreg[i] = (i < d && lane < d) ? Hr[(int64_t)i * d + lane] : 0.0;
+      }
+      __syncwarp();
+      goto iterate;
+    }
+
+    for (int j = lane; j < d; j += 32) x[j] = A.x0[(int64_t)j * A.ldx + s];
     if constexpr (DR > 0) {
 #pragma unroll
       for (int i = 0; i < DR; ++i) hreg[i] = (i == lane) ? 1.0 : 0.0;
@@ -120,17 +224,10 @@ struct BfgsWarp {
     }
     __syncwarp();
 
-    double acc[Obj::NACC];
-    double* TT = T + Obj::NACC * A.bmax * A.tstride;  // term tangents [KT][bmax][tstride]
-    double f0 = eval_batch<Obj>(0, nullptr, d, x, p, T, TT, A.tstride, A.bmax, lane, acc);
+    f0 = evalb(A, 0, nullptr, d, TT, lane, acc);
     f0 = __shfl_sync(kFull, f0, 0);
 #pragma unroll
     for (int a = 0; a < Obj::NACC; ++a) acc[a] = __shfl_sync(kFull, acc[a], 0);
-
-    int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
-    double gnorm = __longlong_as_double(0x7ff0000000000000LL);
-    double ddir = 0.0;
-    bool pending = false;
 
     // ---- iteration 0 prologue: stop probe, first gradient, p = -g
     if (A.stop_flag && *(volatile int*)A.stop_flag) {
@@ -159,6 +256,7 @@ struct BfgsWarp {
     }
 
     PHASE(5);  // prologue: loads, H = I, f(x0), first gradient
+  iterate:
     for (;;) {
       if (gnorm < A.theta) {
         status = ZEUS_CONVERGED;
@@ -168,8 +266,8 @@ struct BfgsWarp {
         status = ZEUS_DIVERGED;
         break;
       }
-      if constexpr (DR > 0) {
-        if (A.k1 > 0 && k == A.k1) {  // straggler: hand over to the CTA-team kernel
+      if constexpr (DR > 0 && NH == 0) {
+        if (A.k1 > 0 && k == A.k1) {  // straggler: hand over to the helper-warp kernel
           promote(A, s, lane, hreg, pending, a_col[0], b_col[0], f0, acc, gnorm, ddir, k,
                   ls_trials, grads, prev_trials);
           return;
@@ -188,8 +286,7 @@ struct BfgsWarp {
           if (lane < B) atab[lane] = alpha_at(A, t0 + lane);
           __syncwarp();
           double accb[Obj::NACC];
-          const double fb =
-              eval_batch<Obj>(B, atab, d, x, p, T, TT, A.tstride, A.bmax, lane, accb);
+          const double fb = evalb(A, B, atab, d, TT, lane, accb);
           bool pass = false;
           if (lane < B) pass = fb <= f0 + A.c1 * atab[lane] * ddir;  // NaN fails
           const unsigned m = __ballot_sync(kFull, pass);
@@ -399,8 +496,10 @@ struct BfgsWarp {
   }
 };
 
-template <class Obj, int DR>
-__global__ void __launch_bounds__(kBfgsWarps * 32, DR > 0 ? ZEUS_MINB : 1) bfgs_warp_kernel(BfgsArgs A) {
+template <class Obj, int DR, int NH = 0>
+__global__ void __launch_bounds__(NH > 0 ? 32 * (NH + 1) : kBfgsWarps * 32,
+                                  NH > 0 ? 1 : (DR > 0 ? ZEUS_MINB : 1))
+    bfgs_warp_kernel(BfgsArgs A) {
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int d = A.d;
@@ -415,8 +514,9 @@ __global__ void __launch_bounds__(kBfgsWarps * 32, DR > 0 ? ZEUS_MINB : 1) bfgs_
     }
   }
   __syncthreads();
-  double* base = sm + A.nalpha + (size_t)wib * A.warp_doubles;
-  BfgsWarp<Obj, DR> W;
+  // one slice per warp (NH == 0) or one slice per CTA (NH > 0)
+  double* base = sm + A.nalpha + (NH > 0 ? (size_t)0 : (size_t)wib * A.warp_doubles);
+  BfgsWarp<Obj, DR, NH> W;
   W.alpha_tab = alpha_tab;
   double* v = base;
   if constexpr (DR == 0) {
@@ -442,13 +542,59 @@ __global__ void __launch_bounds__(kBfgsWarps * 32, DR > 0 ? ZEUS_MINB : 1) bfgs_
   W.gn = v;
   v += d;
   W.T = v;
-  for (;;) {
-    long long s = 0;
-    if (lane == 0) s = (long long)atomicAdd(A.work, 1ull);
-    s = __shfl_sync(kFull, s, 0);
-    if (s >= A.n) break;
-    BfgsWarp<Obj, DR> w = W;  // fresh pointer set per start (run() swaps x/xn, g/gn)
-    w.run(A, s, lane);
+  W.xbuf[0] = W.x;
+  W.xbuf[1] = W.xn;
+  W.task = reinterpret_cast<HelperTask*>(sm + A.nalpha + A.warp_doubles);
+
+  if constexpr (NH == 0) {
+    for (;;) {
+      long long s = 0;
+      if (lane == 0) s = (long long)atomicAdd(A.work, 1ull);
+      s = __shfl_sync(kFull, s, 0);
+      if (s >= A.n) break;
+      BfgsWarp<Obj, DR, NH> w = W;  // fresh pointer set per start (run() swaps x/xn, g/gn)
+      w.run(A, s, lane);
+    }
+  } else if (wib == 0) {  // driving warp
+    const long long nwork = A.resume ? (long long)*A.promo_count : A.n;
+    for (;;) {
+      long long w = 0;
+      if (lane == 0) w = (long long)atomicAdd(A.resume ? A.promo_taken : A.work, 1ull);
+      w = __shfl_sync(kFull, w, 0);
+      if (w >= nwork) break;
+      BfgsWarp<Obj, DR, NH> wk = W;
+      if (A.resume) {
+        const double* rec = A.carry + (size_t)w * A.carry_stride;
+        wk.run(A, (long long)rec[0], lane, rec);
+      } else {
+        wk.run(A, w, lane);
+      }
+    }
+    if (lane == 0) W.task->B = -1;
+    __syncwarp();
+    bar1(32 * (NH + 1));  // A: release the helpers
+  } else {  // helper warps: evaluate term batches until told to exit
+    const int tid = threadIdx.x;
+    const int nt = Obj::nterms(d);
+    double* TT = W.T + Obj::NACC * A.bmax * A.tstride;
+    const double* atab = TT + Obj::KT * A.bmax * A.tstride;
+    for (;;) {
+      bar1(32 * (NH + 1));  // A
+      const int B = W.task->B;
+      if (B < 0) break;
+      const double* x = W.xbuf[W.task->xsel];
+      const int total = (B > 0 ? B : 1) * nt;
+      bool oor = false;
+      if (total > 0)
+        term_pass<Obj, FastMath, 32 * (NH + 1)>(B, nt, total, atab, d, x, W.p, W.T, TT,
+                                               A.tstride, A.bmax, tid, oor);
+      if (bar1_or(32 * (NH + 1), oor)) {  // B
+        if (total > 0)
+          term_pass<Obj, PreciseMath, 32 * (NH + 1)>(B, nt, total, atab, d, x, W.p, W.T, TT,
+                                                    A.tstride, A.bmax, tid, oor);
+        bar1(32 * (NH + 1));
+      }
+    }
   }
 }
 
@@ -526,6 +672,41 @@ static int launch_plan(BfgsArgs A, const BfgsPlan& P, cudaStream_t s) {
   kern<<<grid, P.wpb * 32, P.smem, s>>>(A);
   return check_launch("bfgs_warp_kernel");
 }
+
+// Phase 2 of small-d runs: the promoted stragglers, one CTA (1 + NH warps) each.
+template <class Obj, int DR, int NH>
+static int launch_helpers(BfgsArgs A, const BfgsPlan& P, cudaStream_t s) {
+  auto kern = bfgs_warp_kernel<Obj, DR, NH>;
+  const size_t smem = (P.nalpha + P.warp_doubles + 2) * sizeof(double);
+  int rc = check_cuda(
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+      "cudaFuncSetAttribute(helpers)");
+  if (rc) return rc;
+  int per_sm = 0;
+  rc = check_cuda(
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * (NH + 1), smem),
+      "occupancy(helpers)");
+  if (rc) return rc;
+  const int sms = current_sm_count();
+  if (per_sm < 1 || sms < 1) return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs helpers: no fit");
+  kern<<<per_sm * sms, 32 * (NH + 1), smem, s>>>(A);
+  return check_launch("bfgs_warp_kernel(helpers)");
+}
+
+struct BfgsResumeLaunch {
+  template <class Obj>
+  static int run(BfgsArgs A, cudaStream_t s) {
+    const BfgsPlan P = bfgs_plan(A.d, Obj::NACC, std::max(1, A.d), A.iter_ls);
+    A.warp_doubles = (int)P.warp_doubles;
+    A.ldh = P.ldh;
+    A.tstride = P.tstride;
+    A.bmax = P.bmax;
+    A.nalpha = P.nalpha;
+    if (P.dr == 16) return launch_helpers<Obj, 16, 7>(A, P, s);
+    if (P.dr == 32) return launch_helpers<Obj, 32, 7>(A, P, s);
+    return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs resume: d=%d", A.d);
+  }
+};
 
 struct BfgsLaunch {
   template <class Obj>
@@ -631,7 +812,7 @@ int zeus_bfgs(int obj, int d, int64_t n, const double* x0, int64_t ldx,
     rc = dispatch_objective<BfgsLaunch>(obj, A, s);
     if (rc == ZEUS_OK && A.k1 > 0) {  // phase 2: the promoted stragglers, 8 warps each
       A.resume = 1;
-      rc = launch_bfgs_team(obj, A, s);
+      rc = dispatch_objective<BfgsResumeLaunch>(obj, A, s);
     }
   }
   if (rc == ZEUS_ERR_ARGUMENT) return set_error(rc, "unknown objective id %d", obj);

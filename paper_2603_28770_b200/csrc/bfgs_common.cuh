@@ -88,11 +88,33 @@ struct TrialX {
   __device__ __forceinline__ double operator()(int j) const { return x[j] + alpha * p[j]; }
 };
 
+// Sum of 8 values over a warp, identical in every lane: a transpose-reduce
+// (each level halves the values a lane carries: 4+2+1+1+1 shuffles) followed
+// by 8 broadcasts -- 17 double shuffles instead of 40 for 8 butterflies.
 __device__ __forceinline__ void warp_sum8(double v[8]) {
+  const int lane = threadIdx.x & 31;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  double w4[4], w2[2];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int q = 0; q < 4; ++q) {
+    const double send = b4 ? v[q] : v[q + 4];
+    const double keep = b4 ? v[q + 4] : v[q];
+    w4[q] = keep + __shfl_xor_sync(kFull, send, 16);
+  }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] += __shfl_xor_sync(kFull, v[q], o);
+  for (int q = 0; q < 2; ++q) {
+    const double send = b3 ? w4[q] : w4[q + 2];
+    const double keep = b3 ? w4[q + 2] : w4[q];
+    w2[q] = keep + __shfl_xor_sync(kFull, send, 8);
+  }
+  double w1 = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(kFull, b2 ? w2[0] : w2[1], 4);
+  w1 += __shfl_xor_sync(kFull, w1, 2);
+  w1 += __shfl_xor_sync(kFull, w1, 1);
+  // lane l now holds value index b2 + 2 b3 + 4 b4
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int src = ((q >> 2) & 1) << 4 | ((q >> 1) & 1) << 3 | (q & 1) << 2;
+    v[q] = __shfl_sync(kFull, w1, src);
   }
 }
 

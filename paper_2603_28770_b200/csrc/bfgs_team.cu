@@ -42,11 +42,7 @@ template <int NW>
 __device__ __forceinline__ void cta_sum8(double v[8], double* red, int lane, int warp,
                                          bool w0only) {
   if (!w0only || warp == 0) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] += __shfl_xor_sync(kFull, v[q], o);
-    }
+    warp_sum8(v);
     if (lane == 0) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) red[warp * 8 + q] = v[q];

@@ -49,22 +49,29 @@ struct FastMath {
     oor |= !trig_in_range(x);
     return sincos_fast(x).c;
   }
-  __device__ static __forceinline__ double sin(double x, bool& oor) {
+  __device__ static __forceinline__ SinCos sincos(double x, bool& oor) {
     oor |= !trig_in_range(x);
-    return sincos_fast(x).s;
+    return sincos_fast(x);
   }
 };
 struct PreciseMath {
   __device__ static __forceinline__ double cos(double x, bool&) { return ::cos(x); }
-  __device__ static __forceinline__ double sin(double x, bool&) { return ::sin(x); }
+  __device__ static __forceinline__ SinCos sincos(double x, bool&) {
+    SinCos r;
+    ::sincos(x, &r.s, &r.c);
+    return r;
+  }
 };
 // Single-call policy (PSO, thread-sequential code): fast path, libm fallback.
 struct AutoMath {
   __device__ static __forceinline__ double cos(double x, bool&) {
     return trig_in_range(x) ? sincos_fast(x).c : ::cos(x);
   }
-  __device__ static __forceinline__ double sin(double x, bool&) {
-    return trig_in_range(x) ? sincos_fast(x).s : ::sin(x);
+  __device__ static __forceinline__ SinCos sincos(double x, bool&) {
+    if (trig_in_range(x)) return sincos_fast(x);
+    SinCos r;
+    ::sincos(x, &r.s, &r.c);
+    return r;
   }
 };
 
@@ -78,7 +85,8 @@ template <class M>
 __device__ __forceinline__ double gcos(double x, bool& oor) { return M::cos(x, oor); }
 template <class M>
 __device__ __forceinline__ Dual gcos(Dual x, bool& oor) {
-  return {M::cos(x.r, oor), (-M::sin(x.r, oor)) * x.d};
+  const SinCos sc = M::sincos(x.r, oor);  // one reduction serves value and tangent
+  return {sc.c, (-sc.s) * x.d};
 }
 // float path only rejects negatives; Dual path also rejects 0 (autodiff.py:198-216)
 __device__ __forceinline__ double gsqrt(double x, bool& err) {

@@ -86,12 +86,12 @@ __host__ __device__ __forceinline__ SinCos sincos_fast(double x) {
   SinCos out;
   out.s = (q == 0) ? s : (q == 1) ? c : (q == 2) ? -s : -c;
   out.c = (q == 0) ? c : (q == 1) ? -s : (q == 2) ? -c : s;
-  // tiny arguments: sin x = x (keeps the sign of zero), cos x = 1
+  // tiny arguments: sin x = x (keeps the sign of zero), cos x = 1 (selects,
+  // no branch: keeps independent calls interleavable)
   const double ax = x < 0 ? -x : x;
-  if (ax < 1.4901161193847656e-08) {  // 2^-26
-    out.s = x;
-    out.c = 1.0;
-  }
+  const bool tiny = ax < 1.4901161193847656e-08;  // 2^-26
+  out.s = tiny ? x : out.s;
+  out.c = tiny ? 1.0 : out.c;
   return out;
 }
 

@@ -161,6 +161,30 @@ int zeus_hessian_update(int d, int64_t n, double *H, const double *dx, const dou
 int zeus_bench_dfma(int blocks, int threads, long long iters, double *sink, double *flops_out,
                     void *stream);
 
+/* ---- experiment metrics: bench.py:131-141 count_within on device.
+ * *count += number of points i (SoA x [d][ldx]) with |x_i - optimum|_2 < radius
+ * (optimum: device array of d doubles; *count is accumulated, zero it first). */
+int zeus_count_within(int d, int64_t n, const double *x, int64_t ldx, const double *optimum,
+                      double radius, unsigned long long *count, void *stream);
+
+/* ---- cross-GPU early stop: driver.py:137-202 (_init_worker / _run_parallel's
+ * shared Value('q') counter and Value('i') flag, one per pool).  Here the pool
+ * is one process per GPU: rank 0 creates a stop block in its device memory and
+ * exports a CUDA IPC handle (ZEUS_IPC_HANDLE_BYTES opaque bytes, sent to the
+ * other ranks by the host, e.g. torch.distributed.broadcast_object_list); the
+ * other ranks open it and every rank passes (block, block + 8) as
+ * zeus_bfgs's stop_counter / stop_flag.  The BFGS kernels use system-scope
+ * atomics and volatile flag loads, so the counter is coherent across GPUs
+ * over NVLink / NVSwitch.  Layout: u64 counter at offset 0, i32 flag at 8. */
+#define ZEUS_STOP_BLOCK_BYTES 64
+#define ZEUS_IPC_HANDLE_BYTES 64
+int zeus_stop_block_create(void **block, unsigned char *handle);
+int zeus_stop_block_open(const unsigned char *handle, void **block);
+/* owner = 1 frees the block (creator), 0 unmaps an opened handle */
+int zeus_stop_block_close(void *block, int owner);
+/* zero counter and flag on `stream` (call before the ranks launch) */
+int zeus_stop_block_reset(void *block, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

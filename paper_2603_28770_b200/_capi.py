@@ -66,6 +66,11 @@ _SIGNATURES = {
     "zeus_hessian_update": (_int, [_int, _i64, _vp, _vp, _vp, _vp, _vp]),
     "zeus_bench_dfma": (_int, [_int, _int, ctypes.c_longlong, _vp,
                                ctypes.POINTER(_dbl), _vp]),
+    "zeus_count_within": (_int, [_int, _i64, _vp, _i64, _vp, _dbl, _vp, _vp]),
+    "zeus_stop_block_create": (_int, [ctypes.POINTER(_vp), ctypes.c_char_p]),
+    "zeus_stop_block_open": (_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "zeus_stop_block_close": (_int, [_vp, _int]),
+    "zeus_stop_block_reset": (_int, [_vp, _vp]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 

@@ -488,8 +488,8 @@ struct BfgsWarp {
       if (o.ls_trials) o.ls_trials[s] = ls_trials;
       if (o.grad_evals) o.grad_evals[s] = grads;
       if (status == ZEUS_CONVERGED && A.stop_counter) {
-        const unsigned long long old = atomicAdd(A.stop_counter, 1ull);
-        if ((long long)old + 1 == A.required_c) atomicExch(A.stop_flag, 1);
+        const unsigned long long old = atomicAdd_system(A.stop_counter, 1ull);
+        if ((long long)old + 1 == A.required_c) atomicExch_system(A.stop_flag, 1);
       }
     }
     __syncwarp();
@@ -801,7 +801,9 @@ int zeus_bfgs(int obj, int d, int64_t n, const double* x0, int64_t ldx,
   A.promo_taken = hdr + 2;
   int rc = check_cuda(cudaMemsetAsync(workspace, 0, 3 * sizeof(unsigned long long), s), "memset");
   if (rc) return rc;
-  if (bfgs_team_covers(obj, d) && !getenv_flag("ZEUS_NO_TEAM")) {
+  if (bfgs_wide_covers(obj, d) && !getenv_flag("ZEUS_NO_WIDE")) {
+    rc = launch_bfgs_wide(obj, A, s);
+  } else if (bfgs_team_covers(obj, d) && !getenv_flag("ZEUS_NO_TEAM")) {
     rc = launch_bfgs_team(obj, A, s);
   } else {
     if (promotes(d) && P->iter_bfgs > promotion_k1()) {

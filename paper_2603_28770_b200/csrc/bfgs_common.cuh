@@ -218,4 +218,8 @@ int launch_bfgs_team(int obj, BfgsArgs A, cudaStream_t s);
 bool bfgs_team_covers(int obj, int d);
 int team_phase_cycles(unsigned long long* out, int reset);  // -DZEUS_PHASE_TIMING only
 
+// Launch of the warp-per-start throughput kernel for 32 < d <= 64 (bfgs_wide.cu).
+int launch_bfgs_wide(int obj, BfgsArgs A, cudaStream_t s);
+bool bfgs_wide_covers(int obj, int d);
+
 }  // namespace zeus

@@ -426,8 +426,8 @@ struct BfgsTeam {
       if (o.ls_trials) o.ls_trials[s] = ls_trials;
       if (o.grad_evals) o.grad_evals[s] = grads;
       if (status == ZEUS_CONVERGED && A.stop_counter) {
-        const unsigned long long old = atomicAdd(A.stop_counter, 1ull);
-        if ((long long)old + 1 == A.required_c) atomicExch(A.stop_flag, 1);
+        const unsigned long long old = atomicAdd_system(A.stop_counter, 1ull);
+        if ((long long)old + 1 == A.required_c) atomicExch_system(A.stop_flag, 1);
       }
     }
     __syncthreads();

@@ -4,6 +4,7 @@
 // cross-shard min-loc select (pso.py:73-76 across GPUs).
 #include <stdarg.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "objectives.cuh"
 #include "zeus_internal.h"
@@ -178,6 +179,23 @@ __global__ void minloc_select_kernel(int d, int ncand, const double* cands, doub
   for (int k = threadIdx.x; k < d; k += blockDim.x) gX[k] = cands[(int64_t)win * (d + 2) + 2 + k];
 }
 
+// bench.py:131-141 count_within over SoA final points: |x_i - optimum|_2 < radius
+__global__ void count_within_kernel(int d, int64_t n, const double* x, int64_t ldx,
+                                    const double* opt, double radius, unsigned long long* count) {
+  unsigned c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double e = x[(int64_t)k * ldx + i] - opt[k];
+      s = s + e * e;
+    }
+    c += sqrt(s) < radius ? 1u : 0u;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
 }  // namespace zeus
 
 using namespace zeus;
@@ -258,6 +276,59 @@ int zeus_minloc_select(int d, int ncand, const double* cands, double* gX, double
     return set_error(ZEUS_ERR_ARGUMENT, "zeus_minloc_select: bad arguments");
   minloc_select_kernel<<<1, 128, 0, as_stream(stream)>>>(d, ncand, cands, gX, gbest);
   return check_launch("minloc_select_kernel");
+}
+
+int zeus_count_within(int d, int64_t n, const double* x, int64_t ldx, const double* optimum,
+                      double radius, unsigned long long* count, void* stream) {
+  if (d < 1 || n < 0 || ldx < n || !optimum || !count || (n > 0 && !x))
+    return set_error(ZEUS_ERR_ARGUMENT, "zeus_count_within: bad arguments");
+  if (n == 0) return ZEUS_OK;
+  const int B = 256;
+  int sms = current_sm_count();
+  const int64_t want = (n + B - 1) / B, cap = (int64_t)(sms > 0 ? sms : 148) * 8;
+  count_within_kernel<<<(unsigned)(want < cap ? want : cap), B, 0, as_stream(stream)>>>(
+      d, n, x, ldx, optimum, radius, count);
+  return check_launch("count_within_kernel");
+}
+
+// ---- cross-process early-stop block (driver.py:153-177 across GPUs) --------
+// 64 bytes of cudaMalloc'ed device memory: counter (u64) at 0, flag (i32) at 8.
+// Its own allocation, so the IPC handle maps exactly this block (torch's
+// caching allocator would hand out an offset into a larger segment).
+int zeus_stop_block_create(void** dptr, unsigned char* handle) {
+  if (!dptr || !handle) return set_error(ZEUS_ERR_ARGUMENT, "zeus_stop_block_create");
+  void* p = nullptr;
+  int rc = check_cuda(cudaMalloc(&p, ZEUS_STOP_BLOCK_BYTES), "cudaMalloc(stop block)");
+  if (rc) return rc;
+  rc = check_cuda(cudaMemset(p, 0, ZEUS_STOP_BLOCK_BYTES), "cudaMemset(stop block)");
+  cudaIpcMemHandle_t h;
+  if (!rc) rc = check_cuda(cudaIpcGetMemHandle(&h, p), "cudaIpcGetMemHandle");
+  if (rc) {
+    cudaFree(p);
+    return rc;
+  }
+  memcpy(handle, &h, sizeof(h));
+  *dptr = p;
+  return ZEUS_OK;
+}
+
+int zeus_stop_block_open(const unsigned char* handle, void** dptr) {
+  if (!dptr || !handle) return set_error(ZEUS_ERR_ARGUMENT, "zeus_stop_block_open");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return check_cuda(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess),
+                    "cudaIpcOpenMemHandle");
+}
+
+int zeus_stop_block_close(void* dptr, int owner) {
+  if (!dptr) return ZEUS_OK;
+  return owner ? check_cuda(cudaFree(dptr), "cudaFree(stop block)")
+               : check_cuda(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
+}
+
+int zeus_stop_block_reset(void* dptr, void* stream) {
+  if (!dptr) return set_error(ZEUS_ERR_ARGUMENT, "zeus_stop_block_reset");
+  return check_cuda(cudaMemsetAsync(dptr, 0, 16, as_stream(stream)), "reset stop block");
 }
 
 }  // extern "C"

@@ -102,6 +102,7 @@ class RunStats:
     bfgs_time: float = 0.0      # device seconds, the persistent BFGS kernel
     reduce_time: float = 0.0    # device seconds, reduce_best (+ collectives)
     kernel_launches: int = 0    # our kernels launched by this call
+    n_within: int | None = None  # zeus_run(within=(optimum, radius)): starts inside
 
 
 @dataclass
@@ -218,15 +219,14 @@ def _gather_rows(t: torch.Tensor, per: int, world: int, group) -> torch.Tensor:
     pad = torch.zeros(*lead, per, dtype=t.dtype, device=t.device)
     pad[..., : t.shape[-1]] = t
     flat = pad.reshape(-1, per).contiguous()
-    out = torch.empty((world,) + tuple(flat.shape), dtype=t.dtype, device=t.device)
-    torch.distributed.all_gather_into_tensor(out.view(-1), flat.view(-1), group=group)
+    out = engine.all_gather_flat(flat.view(-1), group).view((world,) + tuple(flat.shape))
     # [world][rows][per] -> [rows][world*per]
     return out.permute(1, 0, 2).reshape(*lead, world * per)
 
 
 def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
              process_group=None, starts: Optional[np.ndarray] = None,
-             gather: bool = True) -> ZeusResult:
+             gather: bool = True, within=None) -> ZeusResult:
     """Run the full pipeline on registered objective ``f`` (driver.py:220-265).
 
     Extensions (keyword-only, defaults reproduce the reference):
@@ -236,6 +236,9 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
       starts        host-supplied BFGS starts [N][dim]: skips PSO (used to
                     decouple BFGS parity from PSO libm flips).
       gather        False keeps per_run local to this rank's shard.
+      within        (optimum, radius): count the starts whose final point lies
+                    within radius of optimum on device (bench.py:131-141),
+                    reported as stats.n_within (summed over ranks).
 
     Early stop: ``deterministic`` or ``required_c == N`` runs every start.
     ``workers == 0`` with ``required_c < N`` reproduces the reference's
@@ -256,9 +259,6 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
     required_c = N if cfg.deterministic else int(cfg.required_c)
     early = required_c < N
     device_stop = early and cfg.workers > 0
-    if device_stop and world > 1:
-        raise NotImplementedError("cross-GPU early stop (workers > 0, required_c < N) is not "
-                                  "implemented yet; use deterministic=True or workers=0")
     stream = torch.cuda.current_stream(dev)
     ev_start, ev_pso, ev_bfgs, ev_end = (torch.cuda.Event(enable_timing=True) for _ in range(4))
     launches0 = engine.LAUNCHES[0]
@@ -295,9 +295,14 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
     out = engine.BfgsBuffers.allocate(d, n, dev)
     params = engine.bfgs_params(cfg.theta, cfg.iter_bfgs, cfg.ls)
     stop = None
-    if device_stop:
+    if device_stop and world == 1:
         stop = (torch.zeros(1, dtype=torch.int64, device=dev),
                 torch.zeros(1, dtype=torch.int32, device=dev))
+    elif device_stop:
+        # one counter/flag for every GPU of the group (driver.py:137-202)
+        blk = engine.StopBlock.get(process_group, dev)
+        blk.arm(process_group, dev)
+        stop = (blk.counter, blk.flag)
     if n > 0:
         engine.run_bfgs(obj, x0.contiguous() if x0.stride(0) != x0.shape[1] else x0, params,
                         out, dev, required_c=required_c, stop=stop)
@@ -316,9 +321,23 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
     else:
         best_dev[0] = math.nan
         best_dev[1] = -1.0
+    n_within = None
+    if within is not None:
+        opt = torch.tensor([float(v) for v in within[0]], dtype=torch.float64, device=dev)
+        if opt.numel() != d:
+            raise ValueError("within: optimum must have dim coordinates")
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        if n > 0:
+            _capi.check(L.zeus_count_within(d, n, out.x_final.data_ptr(), out.x_final.shape[1],
+                                            opt.data_ptr(), float(within[1]), cnt.data_ptr(),
+                                            _device.stream_ptr(dev)), "count_within")
+            engine.LAUNCHES[0] += 1
+        if world > 1:
+            engine.all_reduce_sum(cnt, group=process_group)
+        n_within = cnt
     if world > 1:
         best_dev = engine.gather_candidates(best_dev, process_group)  # resolved on the host
-        torch.distributed.all_reduce(tallies, group=process_group)
+        engine.all_reduce_sum(tallies, group=process_group)
     ev_end.record(stream)
 
     # ---- results to host (part of the end-to-end wall time)
@@ -361,6 +380,11 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
             raise NoValidOptimumError("all runs ended in domain errors")
         bidx = gidx - base
     per_run = OutcomeList(x_host, f_h, gn_h, it_h, st_h, length=m)
+    n_in = None if n_within is None else int(n_within.item())
+    if n_within is not None and m < len(f_h):
+        # sequential early stop reports a prefix: count inside it (host columns)
+        tgt = np.asarray([float(v) for v in within[0]], dtype=np.float64)
+        n_in = int(np.count_nonzero(np.linalg.norm(x_host[:m] - tgt, axis=1) < within[1]))
     if not 0 <= bidx < m:
         # best lives on another rank and per_run is local (gather=False)
         best = None
@@ -372,7 +396,8 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
                      pso_time=ev_start.elapsed_time(ev_pso) / 1e3,
                      bfgs_time=ev_pso.elapsed_time(ev_bfgs) / 1e3,
                      reduce_time=ev_bfgs.elapsed_time(ev_end) / 1e3,
-                     kernel_launches=engine.LAUNCHES[0] - launches0)
+                     kernel_launches=engine.LAUNCHES[0] - launches0,
+                     n_within=n_in)
     return ZeusResult(best=best, per_run=per_run, converged_count=converged_count,
                       wall_time=time.perf_counter() - t0, pso_best_before_bfgs=pso_best,
                       device_time=device_time, stats=stats)

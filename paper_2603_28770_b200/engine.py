@@ -79,9 +79,11 @@ def bfgs_params(theta: float, iter_bfgs: int, ls) -> _capi.BfgsParams:
 
 
 def run_bfgs(obj: int, x0: torch.Tensor, params: _capi.BfgsParams, out: BfgsBuffers,
-             device, required_c: int = 0, stop: Optional[tuple[torch.Tensor, torch.Tensor]] = None,
+             device, required_c: int = 0, stop=None,
              ws: Optional[torch.Tensor] = None) -> None:
-    """Multistart BFGS over the SoA starts ``x0`` [d][n] (bfgs.py:80-156)."""
+    """Multistart BFGS over the SoA starts ``x0`` [d][n] (bfgs.py:80-156).
+    ``stop`` = (counter, flag) as tensors or raw device addresses (the
+    cross-process StopBlock)."""
     d, n = x0.shape
     if n == 0:
         return
@@ -90,7 +92,7 @@ def run_bfgs(obj: int, x0: torch.Tensor, params: _capi.BfgsParams, out: BfgsBuff
         ws = _device.workspace(L.zeus_bfgs_workspace_bytes(d, n), device)
     counter = flag = None
     if stop is not None:
-        counter, flag = stop[0].data_ptr(), stop[1].data_ptr()
+        counter, flag = (v if isinstance(v, int) else v.data_ptr() for v in stop)
     _capi.check(L.zeus_bfgs(obj, d, n, x0.data_ptr(), x0.stride(0), params, int(required_c),
                             counter, flag, out.c_struct(n), ws.data_ptr(),
                             _device.stream_ptr(device)), "bfgs")
@@ -155,15 +157,107 @@ def local_barrier(shard: SwarmShard) -> None:
     shard.select(shard.cand, 1)
 
 
-def gather_candidates(cand: torch.Tensor, group=None) -> torch.Tensor:
-    """All-gather each shard's candidate vector (any device / backend):
-    returns [world * len(cand)] in rank order."""
+def _host_backend(group) -> bool:
+    """gloo (CPU tests, or several processes sharing one GPU) moves CUDA
+    tensors through host memory; NCCL collectives run on device."""
+    import torch.distributed as dist
+
+    return dist.get_backend(group) == "gloo"
+
+
+def all_gather_flat(t: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather equal-size 1-D shards: [world * len(t)] in rank order."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
-    gathered = torch.empty(world * cand.numel(), dtype=cand.dtype, device=cand.device)
-    dist.all_gather_into_tensor(gathered, cand.contiguous(), group=group)
-    return gathered
+    src = t.contiguous()
+    if _host_backend(group) and src.is_cuda:
+        out = torch.empty(world * src.numel(), dtype=src.dtype)
+        dist.all_gather_into_tensor(out, src.cpu(), group=group)
+        return out.to(src.device)
+    out = torch.empty(world * src.numel(), dtype=src.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src, group=group)
+    return out
+
+
+def all_reduce_sum(t: torch.Tensor, group=None) -> None:
+    """In-place sum over ranks (status tallies)."""
+    import torch.distributed as dist
+
+    if _host_backend(group) and t.is_cuda:
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
+
+
+def gather_candidates(cand: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather each shard's candidate vector (any device / backend):
+    returns [world * len(cand)] in rank order."""
+    return all_gather_flat(cand, group)
+
+
+class StopBlock:
+    """The early-stop counter and flag shared by every rank of a process
+    group (driver.py:137-202: the pool's Value('q') counter and Value('i')
+    flag).  Group rank 0 allocates 64 B of its device memory and exports a
+    CUDA IPC handle; the other ranks map it (peer access over NVLink, or the
+    same device when several processes share one GPU).  The BFGS kernels bump
+    the counter with system-scope atomics and poll the flag with volatile
+    loads, so a convergence on any GPU stops every GPU.  One block per
+    (group, device), kept for the life of the process."""
+
+    _cache: dict = {}
+
+    def __init__(self, ptr: int, owner: bool):
+        self.ptr, self.owner = ptr, owner
+
+    @property
+    def counter(self) -> int:
+        return self.ptr
+
+    @property
+    def flag(self) -> int:
+        return self.ptr + 8
+
+    @classmethod
+    def get(cls, group, device) -> "StopBlock":
+        import ctypes
+
+        import torch.distributed as dist
+
+        key = (id(group), device.index)
+        blk = cls._cache.get(key)
+        if blk is not None:
+            return blk
+        L = _capi.lib()
+        rank = dist.get_rank(group)
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        handle = ctypes.create_string_buffer(64)
+        ptr = ctypes.c_void_p()
+        if rank == 0:
+            _capi.check(L.zeus_stop_block_create(ctypes.byref(ptr), handle), "stop block create")
+        box = [bytes(handle.raw) if rank == 0 else None]
+        dist.broadcast_object_list(box, src=src, group=group)
+        if rank != 0:
+            _capi.check(L.zeus_stop_block_open(box[0], ctypes.byref(ptr)), "stop block open")
+        blk = cls(int(ptr.value), rank == 0)
+        cls._cache[key] = blk
+        return blk
+
+    def arm(self, group, device) -> None:
+        """Zero counter and flag once no rank still runs a previous call's
+        kernel, and before any rank launches the next one."""
+        import torch.distributed as dist
+
+        dist.barrier(group=group)
+        if self.owner:
+            stream = torch.cuda.current_stream(device)
+            _capi.check(_capi.lib().zeus_stop_block_reset(self.ptr, stream.cuda_stream),
+                        "stop block reset")
+            stream.synchronize()
+        dist.barrier(group=group)
 
 
 def resolve_minloc(pairs) -> int:

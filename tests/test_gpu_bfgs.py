@@ -60,6 +60,11 @@ def test_matches_reference_golden(golden):
     ("rosenbrock", 50, 16, 2000), ("ackley", 50, 64, 1000), ("rastrigin", 50, 24, 2000),
     ("goldstein_price", 2, 256, 1000), ("rosenbrock", 2, 1024, 1000),
     ("rastrigin", 200, 4, 2000),   # H in HBM (d too large for shared memory)
+    # warp-per-start throughput kernel (32 < d <= 64): register/shared H split,
+    # ragged second column set (d not a multiple of 32), both edges of the range
+    ("rosenbrock", 33, 16, 2000), ("rastrigin", 33, 32, 2000), ("ackley", 40, 32, 1000),
+    ("rosenbrock", 64, 8, 2000), ("rastrigin", 64, 16, 2000), ("ackley", 64, 16, 1000),
+    ("rastrigin", 65, 8, 2000),    # first team-kernel size past the wide kernel
 ])
 def test_matches_oracle(oracle, name, d, n, cap):
     lo, hi = BOXES[name]
@@ -70,6 +75,22 @@ def test_matches_oracle(oracle, name, d, n, cap):
           ref.grad_norm)
     assert np.all(dev["ls"] >= dev["k"])            # >= 1 trial per iteration
     assert np.all(dev["ng"] <= dev["k"] + 1)
+
+
+@pytest.mark.parametrize("name,d,n", [("rosenbrock", 50, 64), ("rastrigin", 50, 128),
+                                       ("ackley", 50, 128)])
+def test_wide_kernel_matches_team_kernel(oracle, monkeypatch, name, d, n):
+    """The warp-per-start (bfgs_wide.cu) and CTA-per-start (bfgs_team.cu)
+    kernels implement the same iteration: identical statuses, minimisers
+    within the stated tolerance of each other."""
+    lo, hi = BOXES[name]
+    starts = oracle.pso(name, d, n, 5, lo, hi, 3).positions
+    wide = device_bfgs(name, starts, 2000)
+    monkeypatch.setenv("ZEUS_NO_WIDE", "1")
+    team = device_bfgs(name, starts, 2000)
+    monkeypatch.delenv("ZEUS_NO_WIDE")
+    assert_outcomes_close(wide["x"], wide["f"], wide["s"], team["x"], team["f"], team["s"],
+                          f"wide vs team {name}", team["gn"])
 
 
 def test_hand_traces(z, golden):

@@ -521,8 +521,30 @@ struct WideStart {
 #define ZEUS_WIDE_MINB 5
 #endif
 
+// Per-objective shape, tuned on B200 (scripts/wide_variants.sh +
+// scripts/phase_probe.py at d = 50): rows of H kept in registers (RR) vs
+// resident starts per SM (2 * MINB warps).  Rosenbrock's cheap terms leave
+// registers for 32 H rows at 8 warps/SM; Rastrigin's trig chains want 10
+// warps/SM and 16 register rows.  (Ackley runs on the team kernel, which is
+// faster for it: its exp/sqrt finish and sincos gradient sit on the critical
+// path of a single warp.)
+template <class Obj>
+struct WideShape {
+  static constexpr int RR = Obj::kId == ZEUS_OBJ_ROSENBROCK ? 32 : 16;
+  static constexpr int MINB = Obj::kId == ZEUS_OBJ_ROSENBROCK ? 4 : 5;
+};
+
+#ifdef ZEUS_WIDE_RR_OVERRIDE
+#define ZEUS_WIDE_RR_OF(Obj) ZEUS_WIDE_RR_OVERRIDE
+#define ZEUS_WIDE_MINB_OF(Obj) ZEUS_WIDE_MINB
+#else
+#define ZEUS_WIDE_RR_OF(Obj) WideShape<Obj>::RR
+#define ZEUS_WIDE_MINB_OF(Obj) WideShape<Obj>::MINB
+#endif
+
 template <class Obj, int RR>
-__global__ void __launch_bounds__(kWideWarps * 32, ZEUS_WIDE_MINB) bfgs_wide_kernel(BfgsArgs A) {
+__global__ void __launch_bounds__(kWideWarps * 32, ZEUS_WIDE_MINB_OF(Obj))
+    bfgs_wide_kernel(BfgsArgs A) {
   extern __shared__ double sm[];
   const int l = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* alpha_tab = sm;
@@ -572,17 +594,14 @@ int launch_wide_rr(BfgsArgs A, cudaStream_t s) {
   return check_launch("bfgs_wide_kernel");
 }
 
-#ifndef ZEUS_WIDE_RR
-#define ZEUS_WIDE_RR 16
-#endif
 
 struct WideLaunch {
   template <class Obj>
   static int run(BfgsArgs A, cudaStream_t s) {
-    if constexpr (Obj::kId == ZEUS_OBJ_GOLDSTEIN_PRICE) {
-      return set_error(ZEUS_ERR_UNSUPPORTED, "wide: goldstein_price is 2-D");
+    if constexpr (Obj::kId == ZEUS_OBJ_GOLDSTEIN_PRICE || Obj::kId == ZEUS_OBJ_ACKLEY) {
+      return set_error(ZEUS_ERR_UNSUPPORTED, "wide: objective runs on another kernel");
     } else {
-      return launch_wide_rr<Obj, ZEUS_WIDE_RR>(A, s);
+      return launch_wide_rr<Obj, ZEUS_WIDE_RR_OF(Obj)>(A, s);
     }
   }
 };
@@ -590,7 +609,7 @@ struct WideLaunch {
 }  // namespace
 
 bool bfgs_wide_covers(int obj, int d) {
-  return obj != ZEUS_OBJ_GOLDSTEIN_PRICE && d > 32 && d <= 64;
+  return (obj == ZEUS_OBJ_ROSENBROCK || obj == ZEUS_OBJ_RASTRIGIN) && d > 32 && d <= 64;
 }
 
 int launch_bfgs_wide(int obj, BfgsArgs A, cudaStream_t s) {

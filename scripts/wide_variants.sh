@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build libzeus variants that differ only in bfgs_wide.cu's tuning macros:
-#   scripts/wide_variants.sh NAME "-DZEUS_WIDE_RR=24 -DZEUS_WIDE_CH=4" ...
+#   scripts/wide_variants.sh NAME "-DZEUS_WIDE_RR_OVERRIDE=24 -DZEUS_WIDE_MINB=4 -DZEUS_WIDE_CH=4" ...
 # (pairs of name + flags); outputs variants/lib_<name>.so
 set -e
 cd "$(dirname "$0")/.."

@@ -128,7 +128,9 @@ def test_two_process_early_stop_semantics(z):
     assert np.sum(s == 2) > 0                     # the rest were stopped
     unstarted = (s == 2) & (k == 0)
     assert np.all(np.isinf(gn[unstarted]))        # never-started runs: |g| = inf
-    assert np.array_equal(s == 0, gn < cfg.theta)
+    # converged <=> |g| < theta, except runs stopped at the probe that precedes
+    # the convergence test (bfgs.py:115-121): those keep their small |g|
+    assert np.array_equal(s == 0, (gn < cfg.theta) & (s != 2))
     # both shards were stopped by the one shared flag (each half has stopped runs)
     half = (cfg.N + 1) // 2
     assert np.any(s[:half] == 2) and np.any(s[half:] == 2)

@@ -547,24 +547,30 @@ __global__ void __launch_bounds__(NH > 0 ? 32 * (NH + 1) : kBfgsWarps * 32,
   W.task = reinterpret_cast<HelperTask*>(sm + A.nalpha + A.warp_doubles);
 
   if constexpr (NH == 0) {
+    const long long nwork = A.resume ? (long long)*A.in_count : A.n;
     for (;;) {
       long long s = 0;
-      if (lane == 0) s = (long long)atomicAdd(A.work, 1ull);
+      if (lane == 0) s = (long long)atomicAdd(A.resume ? A.in_taken : A.work, 1ull);
       s = __shfl_sync(kFull, s, 0);
-      if (s >= A.n) break;
+      if (s >= nwork) break;
       BfgsWarp<Obj, DR, NH> w = W;  // fresh pointer set per start (run() swaps x/xn, g/gn)
-      w.run(A, s, lane);
+      if (A.resume) {  // a start promoted by the thread-per-start kernel
+        const double* rec = A.carry_in + (size_t)s * A.carry_stride;
+        w.run(A, (long long)rec[0], lane, rec);
+      } else {
+        w.run(A, s, lane);
+      }
     }
   } else if (wib == 0) {  // driving warp
-    const long long nwork = A.resume ? (long long)*A.promo_count : A.n;
+    const long long nwork = A.resume ? (long long)*A.in_count : A.n;
     for (;;) {
       long long w = 0;
-      if (lane == 0) w = (long long)atomicAdd(A.resume ? A.promo_taken : A.work, 1ull);
+      if (lane == 0) w = (long long)atomicAdd(A.resume ? A.in_taken : A.work, 1ull);
       w = __shfl_sync(kFull, w, 0);
       if (w >= nwork) break;
       BfgsWarp<Obj, DR, NH> wk = W;
       if (A.resume) {
-        const double* rec = A.carry + (size_t)w * A.carry_stride;
+        const double* rec = A.carry_in + (size_t)w * A.carry_stride;
         wk.run(A, (long long)rec[0], lane, rec);
       } else {
         wk.run(A, w, lane);
@@ -751,16 +757,25 @@ int zeus_debug_phase_cycles(unsigned long long* out, int reset) {
 }
 #endif
 
-static int promotion_k1() {
-  const char* v = getenv("ZEUS_K1");
-  return v ? atoi(v) : 48;
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
 }
+// Tiers for d <= 16 (a start moves on when it is still running at the tier's
+// iteration limit; fixed limits keep results deterministic and shard-
+// invariant): one THREAD per start up to k1t, one WARP per start up to k1,
+// then one CTA (8 warps) per start.  Config 2: p50 = 18, p99 = 40 iterations,
+// ~10 of 65,536 starts run to the 2,000 cap (k1t = 16 measured best of
+// 16/24/32 on config 2).
+static int promotion_k1() { return env_int("ZEUS_K1", 48); }
+// (d <= 4: a lone thread's iteration is short enough to run to the cap)
+static int thread_k1(int d) { return env_int("ZEUS_K1T", d <= 4 ? 0 : 16); }
 static bool promotes(int d) { return d <= 16 && promotion_k1() > 0; }
 
 size_t zeus_bfgs_workspace_bytes(int d, int64_t n) {
   if (d < 1) return kWsHeader;
   size_t extra = 0;
-  if (promotes(d)) extra = (size_t)n * carry_stride_for(d) * sizeof(double);
+  if (promotes(d) || d <= 16) extra = 2 * (size_t)n * carry_stride_for(d) * sizeof(double);
   const BfgsPlan P = bfgs_plan(d, 2, d, 1024);
   if (P.dr > 0 || P.smem_h || bfgs_team_covers(ZEUS_OBJ_RASTRIGIN, d)) return kWsHeader + extra;
   int sms = current_sm_count();
@@ -796,25 +811,48 @@ int zeus_bfgs(int obj, int d, int64_t n, const double* x0, int64_t ldx,
   A.out = *out;
   A.work = (unsigned long long*)workspace;
   A.h_global = (double*)((char*)workspace + kWsHeader);
+  // header: [0] work, [1] tier-1 records written, [2] taken, [3] tier-2
+  // records written, [4] taken
   unsigned long long* hdr = (unsigned long long*)workspace;
-  A.promo_count = hdr + 1;
-  A.promo_taken = hdr + 2;
-  int rc = check_cuda(cudaMemsetAsync(workspace, 0, 3 * sizeof(unsigned long long), s), "memset");
+  int rc = check_cuda(cudaMemsetAsync(workspace, 0, 5 * sizeof(unsigned long long), s), "memset");
   if (rc) return rc;
   if (bfgs_wide_covers(obj, d) && !getenv_flag("ZEUS_NO_WIDE")) {
     rc = launch_bfgs_wide(obj, A, s);
   } else if (bfgs_team_covers(obj, d) && !getenv_flag("ZEUS_NO_TEAM")) {
     rc = launch_bfgs_team(obj, A, s);
   } else {
-    if (promotes(d) && P->iter_bfgs > promotion_k1()) {
-      A.k1 = promotion_k1();
-      A.carry = (double*)((char*)workspace + kWsHeader);
-      A.carry_stride = carry_stride_for(d);
+    const int stride = carry_stride_for(d);
+    double* c1 = (double*)((char*)workspace + kWsHeader);
+    double* c2 = c1 + (size_t)n * stride;
+    const int k1 = promotes(d) ? promotion_k1() : 0;
+    const int k1t = thread_k1(d);
+    const bool use_thread = bfgs_thread_covers(obj, d) && !getenv_flag("ZEUS_NO_THREAD");
+    A.carry_stride = stride;
+    bool warp_tier = true;
+    if (use_thread) {  // tier 1: one thread per start
+      A.k1 = (k1t > 0 && P->iter_bfgs > k1t) ? k1t : 0;
+      A.carry = c1;
+      A.promo_count = hdr + 1;
+      rc = launch_bfgs_thread(obj, A, s);
+      warp_tier = A.k1 > 0;
+      A.resume = 1;  // the warp tier consumes tier-1 records
+      A.carry_in = c1;
+      A.in_count = hdr + 1;
+      A.in_taken = hdr + 2;
     }
-    rc = dispatch_objective<BfgsLaunch>(obj, A, s);
-    if (rc == ZEUS_OK && A.k1 > 0) {  // phase 2: the promoted stragglers, 8 warps each
-      A.resume = 1;
-      rc = dispatch_objective<BfgsResumeLaunch>(obj, A, s);
+    if (rc == ZEUS_OK && warp_tier) {  // tier 2: one warp per start
+      A.k1 = (k1 > 0 && P->iter_bfgs > k1) ? k1 : 0;
+      A.carry = c2;
+      A.promo_count = hdr + 3;
+      rc = dispatch_objective<BfgsLaunch>(obj, A, s);
+      if (rc == ZEUS_OK && A.k1 > 0) {  // tier 3: the stragglers, 8 warps each
+        A.resume = 1;
+        A.k1 = 0;
+        A.carry_in = c2;
+        A.in_count = hdr + 3;
+        A.in_taken = hdr + 4;
+        rc = dispatch_objective<BfgsResumeLaunch>(obj, A, s);
+      }
     }
   }
   if (rc == ZEUS_ERR_ARGUMENT) return set_error(rc, "unknown objective id %d", obj);

@@ -34,9 +34,13 @@ struct BfgsArgs {
   int k1;                          // 0: never promote
   double* carry;                   // [capacity][carry_stride] state records
   int carry_stride;                // doubles per record
-  unsigned long long* promo_count; // records written (phase 1) / taken (phase 2)
-  unsigned long long* promo_taken;
-  int resume;                      // team kernel: 1 = consume carry records
+  unsigned long long* promo_count; // records written to `carry`
+  // resume mode: the kernel consumes carry records written by the previous
+  // tier (thread kernel -> warp kernel -> helper-warp kernel)
+  const double* carry_in;
+  unsigned long long* in_count;    // records available in carry_in
+  unsigned long long* in_taken;    // records claimed
+  int resume;                      // 1 = consume carry_in records
 };
 
 // Carry record layout (doubles): [0] start index, [1] k, [2] ls_trials,
@@ -217,6 +221,10 @@ __device__ __forceinline__ bool grad_needs_slow(const double* xs, int d, int lan
 int launch_bfgs_team(int obj, BfgsArgs A, cudaStream_t s);
 bool bfgs_team_covers(int obj, int d);
 int team_phase_cycles(unsigned long long* out, int reset);  // -DZEUS_PHASE_TIMING only
+
+// Launch of the thread-per-start kernel for d <= 16 (bfgs_thread.cu).
+int launch_bfgs_thread(int obj, BfgsArgs A, cudaStream_t s);
+bool bfgs_thread_covers(int obj, int d);
 
 // Launch of the warp-per-start throughput kernel for 32 < d <= 64 (bfgs_wide.cu).
 int launch_bfgs_wide(int obj, BfgsArgs A, cudaStream_t s);

@@ -477,16 +477,16 @@ __global__ void __launch_bounds__(NW * 32, 1) bfgs_team_kernel(BfgsArgs A) {
     }
   }
   BfgsTeam<Obj, NW, R, S> T{sm};
-  const long long nwork = A.resume ? (long long)*A.promo_count : A.n;
+  const long long nwork = A.resume ? (long long)*A.in_count : A.n;
   for (;;) {
     if (tid == 0)
-      *sm.start = (long long)atomicAdd(A.resume ? A.promo_taken : A.work, 1ull);
+      *sm.start = (long long)atomicAdd(A.resume ? A.in_taken : A.work, 1ull);
     __syncthreads();
     const long long w = *sm.start;
     __syncthreads();
     if (w >= nwork) break;
     if (A.resume) {
-      const double* rec = A.carry + (size_t)w * A.carry_stride;
+      const double* rec = A.carry_in + (size_t)w * A.carry_stride;
       T.run(A, (long long)rec[0], tid, rec);
     } else {
       T.run(A, w, tid, nullptr);

@@ -48,6 +48,14 @@ constexpr int kWideLd = 64;      // row stride of the shared-memory H rows
 #define ZEUS_WIDE_CH 4
 #endif
 constexpr int kCH = ZEUS_WIDE_CH;  // trials evaluated together (independent chains)
+#ifndef ZEUS_WIDE_UFROMP
+#define ZEUS_WIDE_UFROMP 1
+#endif
+#if ZEUS_WIDE_UFROMP
+#define UACC(x)
+#else
+#define UACC(x) x
+#endif
 
 // Term j's coordinate accessor: x(j) -> xj, x(j + 1) -> xj1 (Rosenbrock's
 // neighbour); objectives only ever ask for these two.
@@ -379,14 +387,14 @@ struct WideStart {
           h0[i] = e0;
           h1[i] = e1;
           if (i & 1) {
-            u0b = fma(e0, ra.x, u0b);
+            UACC(u0b = fma(e0, ra.x, u0b));
             w0b = fma(e0, ra.y, w0b);
-            u1b = fma(e1, ra.x, u1b);
+            UACC(u1b = fma(e1, ra.x, u1b));
             w1b = fma(e1, ra.y, w1b);
           } else {
-            u0 = fma(e0, ra.x, u0);
+            UACC(u0 = fma(e0, ra.x, u0));
             w0 = fma(e0, ra.y, w0);
-            u1 = fma(e1, ra.x, u1);
+            UACC(u1 = fma(e1, ra.x, u1));
             w1 = fma(e1, ra.y, w1);
           }
         }
@@ -410,13 +418,13 @@ struct WideStart {
             hr[kWideLd + l] = f0v;
             hr[kWideLd + l + 32] = f1v;
           }
-          u0 = fma(e0, ra.x, u0);
+          UACC(u0 = fma(e0, ra.x, u0));
           w0 = fma(e0, ra.y, w0);
-          u1 = fma(e1, ra.x, u1);
+          UACC(u1 = fma(e1, ra.x, u1));
           w1 = fma(e1, ra.y, w1);
-          u0b = fma(f0v, rc.x, u0b);
+          UACC(u0b = fma(f0v, rc.x, u0b));
           w0b = fma(f0v, rc.y, w0b);
-          u1b = fma(f1v, rc.x, u1b);
+          UACC(u1b = fma(f1v, rc.x, u1b));
           w1b = fma(f1v, rc.y, w1b);
         }
         if (i < d) {
@@ -430,15 +438,24 @@ struct WideStart {
             hr[l] = e0;
             hr[l + 32] = e1;
           }
-          u0b = fma(e0, ra.x, u0b);
+          UACC(u0b = fma(e0, ra.x, u0b));
           w0b = fma(e0, ra.y, w0b);
-          u1b = fma(e1, ra.x, u1b);
+          UACC(u1b = fma(e1, ra.x, u1b));
           w1b = fma(e1, ra.y, w1b);
         }
-        u0 += u0b;
         w0 += w0b;
-        u1 += u1b;
         w1 += w1b;
+#if ZEUS_WIDE_UFROMP
+        // u = H_k dg = H_k g' - H_k g = w + p: p = -H_k g is this iteration's
+        // direction (exact in exact arithmetic), so the pass needs one matvec
+        u0 = w0 + p0;
+        u1 = w1 + p1;
+        (void)u0b;
+        (void)u1b;
+#else
+        u0 += u0b;
+        u1 += u1b;
+#endif
       }
 
       // ---- one 8-value reduction: norms, curvature and the p' scalars

@@ -191,7 +191,7 @@ struct Rastrigin {
   __device__ static double init(int, int d) { return 10.0 * d; }
   template <class M, class T>
   __device__ static T term1(T xi, bool& oor) {
-    return xi * xi - 10.0 * gcos<M>(kTwoPi * xi, oor);
+    return xi * xi - 10.0 * gcos<M>(two_pi() * xi, oor);
   }
   template <class M = AutoMath, class X>
   __device__ static void term(const X& x, int j, int, double t[1], bool& oor) {
@@ -225,7 +225,7 @@ struct Ackley {
   template <class M, class T>
   __device__ static void terms(T xi, T& sq, T& cs, bool& oor) {
     sq = xi * xi;
-    cs = gcos<M>(kTwoPi * xi, oor);
+    cs = gcos<M>(two_pi() * xi, oor);
   }
   template <class M = AutoMath, class X>
   __device__ static void term(const X& x, int j, int, double t[2], bool& oor) {

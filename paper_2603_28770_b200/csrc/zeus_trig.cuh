@@ -15,8 +15,15 @@
 // result is correctly rounded except within a small fraction of an ulp of a
 // rounding boundary; near a zero of the function the absolute error stays
 // below 1e-27 (what matters inside a sum of terms).
-// tests/test_trig.py checks the host build of this file against glibc and
-// mpmath on 2e5 samples.
+// The GPU parity tests compare objective values built on it against the
+// reference / oracle (glibc) values.
+//
+// Code generation: the polynomial and reduction constants live in a
+// __constant__ table, so every DFMA/DMUL takes its constant as a c[] bank
+// operand (immediates would be staged through UMOV pairs -- extra issue
+// slots and false dependencies on the few uniform registers, which kept
+// independent sincos chains from interleaving); rint and the quadrant come
+// from one DADD with 1.5 * 2^52 (no FRND / F2I conversion instructions).
 #pragma once
 
 #ifndef __CUDACC__
@@ -36,11 +43,45 @@ namespace zeus {
 
 constexpr double kTrigMax = 1.0e5;
 
+#ifdef __CUDACC__
+// [0] 2/pi, [1..3] pi/2 = PIO2_1 + 1T + 1TT, [4..9] S1..S6, [10..15] C1..C6,
+// [16] 2 pi (objectives.py:30 _TWO_PI = 2.0 * math.pi, exact doubling)
+static __constant__ double kSinCosTab[17] = {
+    0.6366197723675814,    1.5707963267341256,        6.077100506506192e-11,
+    3.5215598651832e-27,   -1.66666666666666324348e-01, 8.33333333332248946124e-03,
+    -1.98412698298579493134e-04, 2.75573137070700676789e-06, -2.50507602534068634195e-08,
+    1.58969099521155010221e-10,  4.16666666666666019037e-02, -1.38888888888741095749e-03,
+    2.48015872894767294178e-05,  -2.75573143513906633035e-07, 2.08757232129817482790e-09,
+    -1.13596475577881948265e-11, 6.283185307179586};
+#endif
+
+// 2 pi as a constant-bank operand on the device (see "Code generation")
+__host__ __device__ __forceinline__ double two_pi() {
+#ifdef __CUDA_ARCH__
+  return kSinCosTab[16];
+#else
+  return 6.283185307179586;
+#endif
+}
+
 struct SinCos {
   double s, c;
 };
 
 __host__ __device__ __forceinline__ SinCos sincos_fast(double x) {
+#ifdef __CUDA_ARCH__
+  const double INV_PIO2 = kSinCosTab[0], PIO2_1 = kSinCosTab[1], PIO2_1T = kSinCosTab[2],
+               PIO2_1TT = kSinCosTab[3];
+  const double S1 = kSinCosTab[4], S2 = kSinCosTab[5], S3 = kSinCosTab[6], S4 = kSinCosTab[7],
+               S5 = kSinCosTab[8], S6 = kSinCosTab[9];
+  const double C1 = kSinCosTab[10], C2 = kSinCosTab[11], C3 = kSinCosTab[12],
+               C4 = kSinCosTab[13], C5 = kSinCosTab[14], C6 = kSinCosTab[15];
+  // rint(x * 2/pi) by the 1.5 * 2^52 shifter (round-half-even, |.| < 2^51);
+  // the integer's low bits sit in the low mantissa word
+  const double shifted = x * INV_PIO2 + 6755399441055744.0;
+  const double fn = shifted - 6755399441055744.0;
+  const int q = __double2loint(shifted) & 3;
+#else
   constexpr double INV_PIO2 = 0.6366197723675814;  // 0x3fe45f306dc9c883
   // pi/2 = PIO2_1 (33 bits: fn * PIO2_1 is exact for |fn| < 2^20) + 1T + 1TT
   constexpr double PIO2_1 = 1.5707963267341256;     // 0x3ff921fb54400000
@@ -53,10 +94,8 @@ __host__ __device__ __forceinline__ SinCos sincos_fast(double x) {
   constexpr double C1 = 4.16666666666666019037e-02, C2 = -1.38888888888741095749e-03,
                    C3 = 2.48015872894767294178e-05, C4 = -2.75573143513906633035e-07,
                    C5 = 2.08757232129817482790e-09, C6 = -1.13596475577881948265e-11;
-#ifdef __CUDA_ARCH__
-  const double fn = rint(x * INV_PIO2);
-#else
   const double fn = std::nearbyint(x * INV_PIO2);
+  const int q = (int)fn & 3;
 #endif
   // reduced argument as a double-double rh + rl (|fn| < 2^17 here)
   const double r0 = x - fn * PIO2_1;  // exact (Sterbenz)
@@ -82,7 +121,6 @@ __host__ __device__ __forceinline__ SinCos sincos_fast(double x) {
   const double ch = a + t2, cl = t2 - (ch - a);  // |a| >= 0.69 > |t2|
   const double c6 = w * z * fma(w * z, fma(z, C6, C5), fma(z, fma(z, C4, C3), C2));
   const double c = ch + (cl + (al - 0.5 * zl + t2l + c6));
-  const int q = (int)fn & 3;
   SinCos out;
   out.s = (q == 0) ? s : (q == 1) ? c : (q == 2) ? -s : -c;
   out.c = (q == 0) ? c : (q == 1) ? -s : (q == 2) ? -c : s;

@@ -96,9 +96,16 @@ def run_bfgs(obj: int, x0: torch.Tensor, params: _capi.BfgsParams, out: BfgsBuff
     _capi.check(L.zeus_bfgs(obj, d, n, x0.data_ptr(), x0.stride(0), params, int(required_c),
                             counter, flag, out.c_struct(n), ws.data_ptr(),
                             _device.stream_ptr(device)), "bfgs")
-    # small d: warp kernel + the CTA-team kernel for promoted stragglers
-    k1 = int(os.environ.get("ZEUS_K1", "48"))
-    LAUNCHES[0] += 2 if (d <= 16 and k1 > 0 and params.iter_bfgs > k1) else 1
+    # small d: thread-per-start tier, warp-per-start tier for starts still
+    # running at k1t, CTA-team tier for those still running at k1 (bfgs.cu)
+    if d <= 16:
+        k1 = int(os.environ.get("ZEUS_K1", "48"))
+        k1t = int(os.environ.get("ZEUS_K1T", "0" if d <= 4 else "16"))
+        thread = os.environ.get("ZEUS_NO_THREAD", "0") in ("", "0")
+        warp = not thread or (k1t > 0 and params.iter_bfgs > k1t)
+        LAUNCHES[0] += int(thread) + int(warp) + int(warp and k1 > 0 and params.iter_bfgs > k1)
+    else:
+        LAUNCHES[0] += 1
 
 
 class SwarmShard:

@@ -100,6 +100,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def _ncu_traffic(config):
+    """DRAM bytes per launch of the config's BFGS kernels from the committed
+    ncu capture (profiles/ncu_summary.json), or None."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))[config][
+            "dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def measure_fp64_peak(torch, dev):
     """DFMA microbenchmark (csrc/measure.cu): the FP64 roofline denominator."""
     import ctypes
@@ -265,6 +275,7 @@ def main():
                                                      max(1, np.sum(st.iterations))),
                        "roofline": {"bound": "fp64", "achieved": ach, "peak": peak,
                                     "unit": "TFLOP/s", "frac": ach / peak,
+                                    "traffic": _ncu_traffic(key),
                                     "flop_convention": "minimal sparse-tangent"}}
 
     dev_t = maxrank([r["dev"] for r in records])
@@ -281,13 +292,7 @@ def main():
         return
 
     achieved = flops_local / bfgs_local / 1e12  # this rank's kernel, TFLOP/s
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get(args.config, {}).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic = _ncu_traffic(args.config)
     line = {
         "metric": METRIC,
         "value": conv / float(np.sum(dev_t)),
@@ -311,7 +316,10 @@ def main():
                 "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(records[0]["d2h"])},
         "gpu_launches": int(sum(r["launches"] for r in records)),
-        "roofline": {"bound": "fp64", "kernel": "bfgs_warp_kernel", "achieved": achieved,
+        "roofline": {"bound": "fp64",
+                     "kernel": "BFGS tiers of the step (bfgs_thread -> bfgs_warp -> CTA-team "
+                               "straggler kernel); see profiles/*_launches.txt for the shares",
+                     "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "peak_source": "measured DFMA microbenchmark (csrc/measure.cu) on this GPU",

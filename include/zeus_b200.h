@@ -21,8 +21,10 @@
 #ifndef ZEUS_B200_H
 #define ZEUS_B200_H
 
+#ifndef __CUDACC_RTC__
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -74,6 +76,7 @@ typedef struct zeus_bfgs_params {
   double shrink;
 } zeus_bfgs_params;
 
+#ifndef __CUDACC_RTC__  /* NVRTC (user-objective programs) sees only the types above */
 /* ---- library ---------------------------------------------------------- */
 int zeus_abi_version(void);
 const char *zeus_last_error(void);
@@ -184,6 +187,8 @@ int zeus_stop_block_open(const unsigned char *handle, void **block);
 int zeus_stop_block_close(void *block, int owner);
 /* zero counter and flag on `stream` (call before the ranks launch) */
 int zeus_stop_block_reset(void *block, void *stream);
+
+#endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

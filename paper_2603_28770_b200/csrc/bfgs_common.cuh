@@ -2,10 +2,14 @@
 // CTA-per-start (bfgs_team.cu) BFGS kernels: launch arguments, the trial-point
 // accessor, the speculative term pass, gradient helpers.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <algorithm>
+#endif
 
 #include "objectives.cuh"
+#ifndef __CUDACC_RTC__
 #include "zeus_internal.h"
+#endif
 
 namespace zeus {
 
@@ -216,6 +220,7 @@ __device__ __forceinline__ bool grad_needs_slow(const double* xs, int d, int lan
 }
 
 
+#ifndef __CUDACC_RTC__
 // Launch of the CTA-per-start kernel family (bfgs_team.cu).  Returns
 // ZEUS_ERR_UNSUPPORTED when no team shape covers (obj, d).
 int launch_bfgs_team(int obj, BfgsArgs A, cudaStream_t s);
@@ -229,5 +234,7 @@ bool bfgs_thread_covers(int obj, int d);
 // Launch of the warp-per-start throughput kernel for 32 < d <= 64 (bfgs_wide.cu).
 int launch_bfgs_wide(int obj, BfgsArgs A, cudaStream_t s);
 bool bfgs_wide_covers(int obj, int d);
+
+#endif  // __CUDACC_RTC__
 
 }  // namespace zeus

@@ -26,6 +26,10 @@ namespace zeus {
 // ---- dual numbers (autodiff.py:62-173) ------------------------------------
 struct Dual {
   double r, d;
+  Dual() = default;
+  // a float constant is a Dual with zero tangent (autodiff.py:66-68)
+  __host__ __device__ constexpr Dual(double v) : r(v), d(0.0) {}
+  __host__ __device__ constexpr Dual(double rv, double dv) : r(rv), d(dv) {}
 };
 __device__ __forceinline__ Dual operator+(Dual a, Dual b) { return {a.r + b.r, a.d + b.d}; }
 __device__ __forceinline__ Dual operator+(Dual a, double s) { return {a.r + s, a.d}; }
@@ -126,6 +130,7 @@ __device__ __forceinline__ double tangent<Dual>(const Dual& v) { return v.d; }
 
 // objectives.py:33-45  (total = total + (a*a + 100*(b*b)), a = 1-x_i, b = x_{i+1}-x_i^2)
 struct Rosenbrock {
+  static constexpr bool kOorIsError = false;  // oor = trig range, not a DomainError
   static constexpr int kId = ZEUS_OBJ_ROSENBROCK;
   static constexpr int NACC = 1;
   __host__ __device__ static int nterms(int d) { return d - 1; }
@@ -185,6 +190,7 @@ struct Rosenbrock {
 
 // objectives.py:48-61  (total = 10 d; total = total + (x*x - 10 cos(2 pi x)))
 struct Rastrigin {
+  static constexpr bool kOorIsError = false;  // oor = trig range, not a DomainError
   static constexpr int kId = ZEUS_OBJ_RASTRIGIN;
   static constexpr int NACC = 1;
   __host__ __device__ static int nterms(int d) { return d; }
@@ -218,6 +224,7 @@ struct Rastrigin {
 
 // objectives.py:64-85
 struct Ackley {
+  static constexpr bool kOorIsError = false;  // oor = trig range, not a DomainError
   static constexpr int kId = ZEUS_OBJ_ACKLEY;
   static constexpr int NACC = 2;  // sum_sq, sum_cos
   __host__ __device__ static int nterms(int d) { return d; }
@@ -267,6 +274,7 @@ struct Ackley {
 
 // objectives.py:88-113 (d == 2 only; validated on the host)
 struct GoldsteinPrice {
+  static constexpr bool kOorIsError = false;  // oor = trig range, not a DomainError
   static constexpr int kId = ZEUS_OBJ_GOLDSTEIN_PRICE;
   static constexpr int NACC = 1;
   __host__ __device__ static int nterms(int) { return 1; }
@@ -346,6 +354,7 @@ __device__ __forceinline__ double value_seq(const X& x, int d, double acc[Obj::N
   return Obj::finish(acc, d, err);
 }
 
+#ifndef __CUDACC_RTC__
 // Dispatch helper: calls F::template run<Obj>(args...) for the objective id.
 template <class F, class... A>
 __host__ int dispatch_objective(int obj, A&&... args) {
@@ -357,5 +366,7 @@ __host__ int dispatch_objective(int obj, A&&... args) {
     default: return ZEUS_ERR_ARGUMENT;
   }
 }
+
+#endif  // __CUDACC_RTC__
 
 }  // namespace zeus

@@ -1,0 +1,193 @@
+// pso_kernels.cuh -- device code of the particle-swarm phase (pso.py:79-164):
+// included by pso.cu (registered objectives) and by the NVRTC program of a
+// user objective (plugin.cu), which instantiates the same kernels.
+//
+// One thread per particle; swarm arrays are SoA [d][ld] so that coordinate k
+// of consecutive particles is one coalesced 256-B transaction per warp.  The
+// uniform draws come straight from the counter-based Philox stream of the
+// particle's GLOBAL index (no RNG state in HBM); every update is evaluated
+// in the reference's numpy order without contraction, so the swarm is
+// bit-identical to init_swarm/update_swarm whenever libm agrees (always for
+// Rosenbrock and Goldstein-Price).  The objective is folded in the same pass
+// that produces x' (no second read of the position), then the personal best
+// is updated under the strict '<' rule and a warp-shuffle + shared-memory
+// block argmin leaves one (f, index) per block; a tiny finalize kernel turns
+// those into this shard's candidate [f, idx, x...] (pso.py:73-76).
+#pragma once
+#include "objectives.cuh"
+
+namespace zeus {
+
+constexpr int kPsoBlock = 256;
+
+// Streaming accumulator: feeds coordinates in order, reproduces value_seq.
+// Generic accumulator (user objectives, d <= kStreamMax): buffers the
+// coordinates, evaluates Obj's sequential value at the end.
+constexpr int kStreamMax = 64;
+template <class Obj>
+struct StreamAcc {
+  double xs[kStreamMax];
+  int k = 0;
+  __device__ void push(double x) { xs[k++] = x; }
+  __device__ double result(int d) {
+    double acc[Obj::NACC];
+    bool err = false;
+    const double f = value_seq<Obj>(DenseX{xs}, d, acc, err);
+    return err ? __longlong_as_double(0x7ff8000000000000LL) : f;
+  }
+};
+
+template <>
+struct StreamAcc<Rosenbrock> {
+  double total = 0.0, prev = 0.0;
+  int k = 0;
+  __device__ void push(double x) {
+    if (k > 0) total = total + Rosenbrock::term2<double>(prev, x);
+    prev = x;
+    ++k;
+  }
+  __device__ double result(int) { return total; }
+};
+template <>
+struct StreamAcc<Rastrigin> {
+  double total;
+  __device__ explicit StreamAcc(int d = 0) : total(10.0 * d) {}
+  __device__ void push(double x) {
+    bool oor = false;
+    total = total + Rastrigin::term1<AutoMath, double>(x, oor);
+  }
+  __device__ double result(int) { return total; }
+};
+template <>
+struct StreamAcc<Ackley> {
+  double sq = 0.0, cs = 0.0;
+  __device__ void push(double x) {
+    double a, b;
+    bool oor = false;
+    Ackley::terms<AutoMath, double>(x, a, b, oor);
+    sq = sq + a;
+    cs = cs + b;
+  }
+  __device__ double result(int d) {
+    bool err = false;
+    return Ackley::outer<double>(sq, cs, d, err);
+  }
+};
+template <>
+struct StreamAcc<GoldsteinPrice> {
+  double x1 = 0.0, v = 0.0;
+  int k = 0;
+  __device__ void push(double x) {
+    if (k == 0) x1 = x;
+    else v = GoldsteinPrice::eval<double>(x1, x);
+    ++k;
+  }
+  __device__ double result(int) { return v; }
+};
+
+template <class Obj>
+__device__ __forceinline__ StreamAcc<Obj> make_acc(int d) {
+  if constexpr (Obj::kId == ZEUS_OBJ_RASTRIGIN) return StreamAcc<Obj>(d);
+  else return StreamAcc<Obj>();
+}
+
+// init_swarm: positions U[lo,hi)^d from draws 0..d-1, velocities U[-vr,vr)^d
+// from draws d..2d-1 (pso.py:101-109); pbest = x; pval = f(x).
+template <class Obj>
+__global__ void __launch_bounds__(kPsoBlock)
+    pso_init_kernel(int d, int64_t n, int64_t i0, uint64_t seed, double lower, double range,
+                    double vlow, double vrange, double* __restrict__ x, double* __restrict__ v,
+                    double* __restrict__ p, double* __restrict__ pval, int64_t ld,
+                    double* blk_f, long long* blk_i) {
+  const int64_t i = blockIdx.x * (int64_t)kPsoBlock + threadIdx.x;
+  double bf = 0.0;
+  long long bi = -1;
+  if (i < n) {
+    PhiloxCursor cur(seed, (uint64_t)(i0 + i));
+    StreamAcc<Obj> acc = make_acc<Obj>(d);
+    for (int k = 0; k < d; ++k) {
+      const double xk = uniform_draw(cur.at((uint64_t)k), lower, range);
+      x[(int64_t)k * ld + i] = xk;
+      p[(int64_t)k * ld + i] = xk;
+      acc.push(xk);
+    }
+    for (int k = 0; k < d; ++k)
+      v[(int64_t)k * ld + i] = uniform_draw(cur.at((uint64_t)(d + k)), vlow, vrange);
+    const double f = acc.result(d);
+    pval[i] = f;
+    bf = f;
+    bi = i0 + i;
+  }
+  block_argmin<kPsoBlock>(bf, bi);
+  if (threadIdx.x == 0) {
+    blk_f[blockIdx.x] = bf;
+    blk_i[blockIdx.x] = bi;
+  }
+}
+
+// update_swarm sweep s: r1 = draws 2d(s+1)+k, r2 = draws 2d(s+1)+d+k;
+// v' = w v + c1 r1 (p - x) + c2 r2 (g - x); x' = x + v' (pso.py:143-163).
+template <class Obj>
+__global__ void __launch_bounds__(kPsoBlock)
+    pso_sweep_kernel(int d, int64_t n, int64_t i0, uint64_t seed, uint64_t k0, double w,
+                     double c1, double c2, double* __restrict__ x, double* __restrict__ v,
+                     double* __restrict__ p, double* __restrict__ pval, int64_t ld,
+                     const double* __restrict__ gX, double* blk_f, long long* blk_i) {
+  const int64_t i = blockIdx.x * (int64_t)kPsoBlock + threadIdx.x;
+  double bf = 0.0;
+  long long bi = -1;
+  if (i < n) {
+    PhiloxCursor c_r1(seed, (uint64_t)(i0 + i)), c_r2(seed, (uint64_t)(i0 + i));
+    StreamAcc<Obj> acc = make_acc<Obj>(d);
+    for (int k = 0; k < d; ++k) {
+      const double r1 = uniform_draw(c_r1.at(k0 + (uint64_t)k), 0.0, 1.0);
+      const double r2 = uniform_draw(c_r2.at(k0 + (uint64_t)(d + k)), 0.0, 1.0);
+      const int64_t o = (int64_t)k * ld + i;
+      const double xk = x[o], vk = v[o], pk = p[o], gk = __ldg(gX + k);
+      const double nv = w * vk + c1 * r1 * (pk - xk) + c2 * r2 * (gk - xk);
+      const double nx = xk + nv;
+      v[o] = nv;
+      x[o] = nx;
+      acc.push(nx);
+    }
+    const double f = acc.result(d);
+    double best = pval[i];
+    if (f < best) {  // strict: ties keep the old personal best (pso.py:161)
+      best = f;
+      pval[i] = f;
+      for (int k = 0; k < d; ++k) p[(int64_t)k * ld + i] = x[(int64_t)k * ld + i];
+    }
+    bf = best;
+    bi = i0 + i;
+  }
+  block_argmin<kPsoBlock>(bf, bi);
+  if (threadIdx.x == 0) {
+    blk_f[blockIdx.x] = bf;
+    blk_i[blockIdx.x] = bi;
+  }
+}
+
+// Reduce block partials -> this shard's candidate [f, idx, pbest[:, idx]].
+__global__ void __launch_bounds__(kPsoBlock)
+    pso_finalize_kernel(int d, int nb, int64_t i0, const double* __restrict__ p, int64_t ld,
+                        const double* blk_f, const long long* blk_i, double* cand) {
+  __shared__ long long win;
+  double bf = 0.0;
+  long long bi = -1;
+  for (int b = threadIdx.x; b < nb; b += kPsoBlock)
+    if (argmin_better(blk_f[b], blk_i[b], bf, bi)) {
+      bf = blk_f[b];
+      bi = blk_i[b];
+    }
+  block_argmin<kPsoBlock>(bf, bi);
+  if (threadIdx.x == 0) {
+    win = bi;
+    cand[0] = bf;
+    cand[1] = (double)bi;
+  }
+  __syncthreads();
+  const long long li = win - i0;
+  for (int k = threadIdx.x; k < d; k += kPsoBlock) cand[2 + k] = p[(int64_t)k * ld + li];
+}
+
+}  // namespace zeus

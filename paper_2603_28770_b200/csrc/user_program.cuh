@@ -1,0 +1,68 @@
+// user_program.cuh -- the tail of a user objective's NVRTC program
+// (plugin.cu): adapts the user's `objective<T>(x, d, data, err)` to the
+// framework's objective interface (objectives.cuh) and pulls in the PSO and
+// thread-per-start BFGS kernels, which NVRTC then instantiates for UserObj.
+// Compiled only by NVRTC, with -DZEUS_USER_D=<d> (the problem dimension, so
+// every per-coordinate array is sized exactly).
+#pragma once
+#include "bfgs_thread.cuh"
+#include "pso_kernels.cuh"
+
+namespace zeus {
+
+__device__ const double* zeus_user_data;  // plugin data array (set by the host)
+
+// coordinate k seeded: x(i) as a Dual with tangent [i == k]
+template <class X>
+struct SeedX {
+  const X& x;
+  int k;
+  __device__ __forceinline__ Dual operator()(int i) const { return Dual{x(i), i == k ? 1.0 : 0.0}; }
+};
+struct PlainX {
+  const double* p;
+  __device__ __forceinline__ double operator()(int i) const { return p[i]; }
+};
+
+// The whole objective is one "term"; its tangents are the d partials from d
+// seeded Dual passes (the reference's forward_gradient).  Domain errors come
+// back through the `oor` flag (kOorIsError): the BFGS kernel turns them into
+// the domain_error status at the old iterate, as bfgs.py does.
+struct UserObj {
+  static constexpr int kId = 100;
+  static constexpr int NACC = 1;
+  static constexpr int KT = ZEUS_USER_D;
+  static constexpr bool kOorIsError = true;
+  __host__ __device__ static int nterms(int) { return 1; }
+  __device__ static double init(int, int) { return 0.0; }
+  __device__ static double finish(const double acc[1], int, bool&) { return acc[0]; }
+  template <class M = AutoMath, class X>
+  __device__ static void term(const X& x, int, int d, double t[1], bool& oor) {
+    t[0] = objective<double>(x, d, zeus_user_data, oor);
+  }
+  template <class M, class X>
+  __device__ static void term_tan(const X& x, int, int d, double t[1], double tan[KT], bool& oor) {
+    t[0] = objective<double>(x, d, zeus_user_data, oor);
+#pragma unroll 1
+    for (int k = 0; k < KT; ++k)
+      tan[k] = k < d ? objective<Dual>(SeedX<X>{x, k}, d, zeus_user_data, oor).d : 0.0;
+  }
+  template <class TA>
+  __device__ static double grad_from_tan(const TA& tan, int i, int, const double*, bool&) {
+    return tan(0, i);
+  }
+};
+
+// f of n points (SoA [d][ldx]); NaN where the objective raises DomainError
+__global__ void user_value_kernel(int d, int64_t n, const double* x, int64_t ldx, double* f) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xs[ZEUS_USER_D];
+  for (int k = 0; k < d; ++k) xs[k] = x[(int64_t)k * ldx + i];
+  bool err = false;
+  double t[1];
+  UserObj::term(PlainX{xs}, 0, d, t, err);
+  f[i] = err ? __longlong_as_double(0x7ff8000000000000LL) : t[0];
+}
+
+}  // namespace zeus

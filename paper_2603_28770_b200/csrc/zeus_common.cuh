@@ -6,8 +6,18 @@
 // BFGS linear algebra wants fused multiply-adds (the reference's OpenBLAS
 // order is implementation-defined anyway) they are written as explicit fma().
 #pragma once
+#ifdef __CUDACC_RTC__
+// NVRTC (user objectives, plugin.cu): no host headers
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#else
 #include <cuda_runtime.h>
 #include <stdint.h>
+#endif
 
 #include "../../include/zeus_b200.h"
 

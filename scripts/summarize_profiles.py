@@ -115,6 +115,7 @@ def main():
         print("\n".join(lines))
     summ_path = os.path.join(prof, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
+    fresh = {}
     for rep in sorted(glob.glob(os.path.join(args.src, "*.ncu-rep"))):
         for m in raw_metrics(rep):
             kname = m["kernel"].split("(")[0]
@@ -129,14 +130,20 @@ def main():
             safe = "".join(c if c.isalnum() else "_" for c in short)[:60].strip("_")
             fn = os.path.join(prof, f"{args.tag}_ncu_{safe}.txt")
             open(fn, "w").write("\n".join(lines) + "\n")
-            print("\n".join(lines))
-            if "dram__bytes_read.sum" in m:
+            try:
+                print("\n".join(lines))
+            except BrokenPipeError:
+                pass
+            if "dram__bytes_read.sum" in m and short.startswith("bfgs"):
+                # the BFGS tiers of one step together (bench.py's roofline spans them)
                 rd = to_bytes(*m["dram__bytes_read.sum"])
                 wr = to_bytes(*m["dram__bytes_write.sum"])
-                summ.setdefault(args.config, {})
-                if short.startswith("bfgs") or "kernel" not in summ[args.config]:
-                    summ[args.config] = {"kernel": short, "dram_bytes_per_launch": rd + wr,
-                                         "source": os.path.basename(fn)}
+                e = fresh.setdefault(args.config, {"kernels": [], "dram_bytes_per_launch": 0.0,
+                                                   "sources": []})
+                e["kernels"].append(short)
+                e["dram_bytes_per_launch"] += rd + wr
+                e["sources"].append(os.path.basename(fn))
+    summ.update(fresh)
     json.dump(summ, open(summ_path, "w"), indent=1)
 
 

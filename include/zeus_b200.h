@@ -188,6 +188,37 @@ int zeus_stop_block_close(void *block, int owner);
 /* zero counter and flag on `stream` (call before the ranks launch) */
 int zeus_stop_block_reset(void *block, void *stream);
 
+/* ---- user objectives: the reference's generic-scalar user callables
+ * (pkg/README.md:70-87, autodiff.py) as device source, compiled at run time
+ * with NVRTC together with this library's PSO and thread-per-start BFGS
+ * kernels.  Contract of `source`: csrc/user_objective.cuh.  1 <= d <= 16.
+ * include_dir: the csrc/ directory holding the kernel headers.  The handle
+ * is bound to the CUDA context current at compile time. */
+int zeus_user_compile(const char *source, int d, const char *include_dir, void **handle);
+const char *zeus_user_compile_log(void); /* NVRTC log of the last compile on this thread */
+int zeus_user_free(void *handle);
+int zeus_user_dim(void *handle);
+/* the objective's `data` argument (device array or NULL); stream-ordered */
+int zeus_user_set_data(void *handle, const double *data, void *stream);
+/* objectives.py-style evaluation of n points (SoA [d][ldx]); NaN where the
+ * objective raises DomainError */
+int zeus_user_value(void *handle, int64_t n, const double *x, int64_t ldx, double *f,
+                    void *stream);
+/* init_swarm / update_swarm (pso.py:79-164) -- as zeus_pso_init/_sweep */
+int zeus_user_pso_init(void *handle, int64_t n, int64_t i0, uint64_t seed, double lower,
+                       double upper, double *x, double *v, double *pbest, double *pval,
+                       int64_t ld, double *cand, void *workspace, void *stream);
+int zeus_user_pso_sweep(void *handle, int64_t n, int64_t i0, uint64_t seed, int sweep,
+                        double w, double c1, double c2, double *x, double *v, double *pbest,
+                        double *pval, int64_t ld, const double *gX, double *cand,
+                        void *workspace, void *stream);
+/* bfgs_run over n starts (bfgs.py:80-156) -- as zeus_bfgs */
+size_t zeus_user_bfgs_workspace_bytes(void);
+int zeus_user_bfgs(void *handle, int64_t n, const double *x0, int64_t ldx,
+                   const zeus_bfgs_params *params, int64_t required_c,
+                   unsigned long long *stop_counter, int *stop_flag, zeus_bfgs_out *out,
+                   void *workspace, void *stream);
+
 #endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus

@@ -67,6 +67,19 @@ _SIGNATURES = {
     "zeus_bench_dfma": (_int, [_int, _int, ctypes.c_longlong, _vp,
                                ctypes.POINTER(_dbl), _vp]),
     "zeus_count_within": (_int, [_int, _i64, _vp, _i64, _vp, _dbl, _vp, _vp]),
+    "zeus_user_compile": (_int, [ctypes.c_char_p, _int, ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "zeus_user_compile_log": (ctypes.c_char_p, []),
+    "zeus_user_free": (_int, [_vp]),
+    "zeus_user_dim": (_int, [_vp]),
+    "zeus_user_set_data": (_int, [_vp, _vp, _vp]),
+    "zeus_user_value": (_int, [_vp, _i64, _vp, _i64, _vp, _vp]),
+    "zeus_user_pso_init": (_int, [_vp, _i64, _i64, _u64, _dbl, _dbl, _vp, _vp, _vp, _vp, _i64,
+                                  _vp, _vp, _vp]),
+    "zeus_user_pso_sweep": (_int, [_vp, _i64, _i64, _u64, _int, _dbl, _dbl, _dbl, _vp, _vp, _vp,
+                                   _vp, _i64, _vp, _vp, _vp, _vp]),
+    "zeus_user_bfgs_workspace_bytes": (_sz, []),
+    "zeus_user_bfgs": (_int, [_vp, _i64, _vp, _i64, ctypes.POINTER(BfgsParams), _i64, _vp, _vp,
+                              ctypes.POINTER(BfgsOut), _vp, _vp]),
     "zeus_stop_block_create": (_int, [ctypes.POINTER(_vp), ctypes.c_char_p]),
     "zeus_stop_block_open": (_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "zeus_stop_block_close": (_int, [_vp, _int]),

@@ -128,7 +128,9 @@ def bfgs_run(
     return full
 
 
-def _f_at(obj: int, x: np.ndarray, dev) -> float:
+def _f_at(obj, x: np.ndarray, dev) -> float:
+    if not isinstance(obj, int):  # user objective
+        return float(obj.values(x.reshape(1, -1))[0])
     xs = torch.from_numpy(x.reshape(-1, 1).copy()).to(dev)
     out = torch.empty(1, dtype=torch.float64, device=dev)
     _capi.check(_capi.lib().zeus_objective_value(obj, x.shape[0], 1, xs.data_ptr(), 1,

@@ -88,11 +88,21 @@ def run_bfgs(obj: int, x0: torch.Tensor, params: _capi.BfgsParams, out: BfgsBuff
     if n == 0:
         return
     L = _capi.lib()
-    if ws is None:
-        ws = _device.workspace(L.zeus_bfgs_workspace_bytes(d, n), device)
     counter = flag = None
     if stop is not None:
         counter, flag = (v if isinstance(v, int) else v.data_ptr() for v in stop)
+    if not isinstance(obj, int):  # user objective (plugin.DeviceObjective)
+        if ws is None:
+            ws = _device.workspace(L.zeus_user_bfgs_workspace_bytes(), device)
+        sp = _device.stream_ptr(device)
+        obj.bind(sp)
+        _capi.check(L.zeus_user_bfgs(obj.handle, n, x0.data_ptr(), x0.stride(0), params,
+                                     int(required_c), counter, flag, out.c_struct(n),
+                                     ws.data_ptr(), sp), "bfgs (user objective)")
+        LAUNCHES[0] += 1
+        return
+    if ws is None:
+        ws = _device.workspace(L.zeus_bfgs_workspace_bytes(d, n), device)
     _capi.check(L.zeus_bfgs(obj, d, n, x0.data_ptr(), x0.stride(0), params, int(required_c),
                             counter, flag, out.c_struct(n), ws.data_ptr(),
                             _device.stream_ptr(device)), "bfgs")
@@ -131,20 +141,29 @@ class SwarmShard:
 
     def init(self, lower: float, upper: float) -> None:
         """init_swarm (pso.py:79-120) for this shard."""
-        _capi.check(_capi.lib().zeus_pso_init(
-            self.obj, self.d, self.n, self.i0, self.seed, float(lower), float(upper),
-            self.x.data_ptr(), self.v.data_ptr(), self.p.data_ptr(), self.pval.data_ptr(),
-            self.n, self.cand.data_ptr(), self.ws.data_ptr(), self._stream()), "pso_init")
+        L = _capi.lib()
+        tail = (self.n, self.i0, self.seed, float(lower), float(upper), self.x.data_ptr(),
+                self.v.data_ptr(), self.p.data_ptr(), self.pval.data_ptr(), self.n,
+                self.cand.data_ptr(), self.ws.data_ptr(), self._stream())
+        if isinstance(self.obj, int):
+            _capi.check(L.zeus_pso_init(self.obj, self.d, *tail), "pso_init")
+        else:
+            self.obj.bind(self._stream())
+            _capi.check(L.zeus_user_pso_init(self.obj.handle, *tail), "pso_init (user)")
         LAUNCHES[0] += 2
         self.sweeps_done = 0
 
     def sweep(self, w: float, c1: float, c2: float) -> None:
         """One update_swarm sweep (pso.py:123-164) using gX of the previous barrier."""
-        _capi.check(_capi.lib().zeus_pso_sweep(
-            self.obj, self.d, self.n, self.i0, self.seed, self.sweeps_done, float(w), float(c1),
-            float(c2), self.x.data_ptr(), self.v.data_ptr(), self.p.data_ptr(),
-            self.pval.data_ptr(), self.n, self.gX.data_ptr(), self.cand.data_ptr(),
-            self.ws.data_ptr(), self._stream()), "pso_sweep")
+        tail = (self.n, self.i0, self.seed, self.sweeps_done, float(w), float(c1), float(c2),
+                self.x.data_ptr(), self.v.data_ptr(), self.p.data_ptr(), self.pval.data_ptr(),
+                self.n, self.gX.data_ptr(), self.cand.data_ptr(), self.ws.data_ptr(),
+                self._stream())
+        if isinstance(self.obj, int):
+            _capi.check(_capi.lib().zeus_pso_sweep(self.obj, self.d, *tail), "pso_sweep")
+        else:
+            _capi.check(_capi.lib().zeus_user_pso_sweep(self.obj.handle, *tail),
+                        "pso_sweep (user)")
         LAUNCHES[0] += 2
         self.sweeps_done += 1
 

@@ -63,6 +63,9 @@ def armijo_search(
     g = np.asarray(g, dtype=np.float64)
     d = x.shape[0]
     obj = objective_id(f, d)
+    if not isinstance(obj, int):
+        raise NotImplementedError(f"armijo_search of a user DeviceObjective: call it through "
+                                  "bfgs_run / zeus_run (its gradient runs inside the BFGS kernel)")
     ddir = float(np.dot(g, p))
     if ddir >= 0.0:
         log.debug("line search entered with non-descent direction (g.p=%g)", ddir)

@@ -132,8 +132,10 @@ def get_objective(name: str, dim: int = 2) -> ObjectiveSpec:
                          gradient_continuous=entry["gradient_continuous"])
 
 
-def objective_id(f, dim: int | None = None) -> int:
-    """Device objective id of a registered callable.
+def objective_id(f, dim: int | None = None):
+    """Device objective id of a registered callable (a ``DeviceObjective``
+    user plug-in is returned as itself: the engine launches its NVRTC
+    module instead of the built-in kernels).
 
     Accepts this package's functions, ``ObjectiveSpec`` objects, registry
     names, and the reference package's own functions (matched by module and
@@ -142,6 +144,14 @@ def objective_id(f, dim: int | None = None) -> int:
     fallback.  Goldstein-Price at ``dim != 2`` raises ``ValueError`` like the
     reference's evaluation would (objectives.py:92-93).
     """
+    from .plugin import DeviceObjective
+
+    if isinstance(f, ObjectiveSpec) and isinstance(f.fn, DeviceObjective):
+        f = f.fn
+    if isinstance(f, DeviceObjective):  # user objective: the plugin stands in for the id
+        if dim is not None and dim != f.dim:
+            raise ValueError(f"{f.name} was compiled for dim={f.dim}, not {dim}")
+        return f
     name = None
     if isinstance(f, ObjectiveSpec):
         name = f.name

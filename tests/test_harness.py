@@ -100,7 +100,7 @@ def test_cli_config_errors(capsys):
     assert cli.main([]) == cli.EXIT_CONFIG                       # usage error -> 1, not 2
     assert cli.main(["run", "--objective", "nope"]) == cli.EXIT_CONFIG
     assert cli.main(["run", "--objective", "goldstein_price", "--dim", "3"]) == cli.EXIT_CONFIG
-    assert cli.main(["fit", "--demo"]) == cli.EXIT_CONFIG
+    assert cli.main(["fit"]) == cli.EXIT_CONFIG                  # needs --data or --demo
     assert cli.main(["bench", "--plan", "/nonexistent.ini", "--seed", "1"]) == cli.EXIT_IO
 
 

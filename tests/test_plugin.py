@@ -1,0 +1,138 @@
+"""User objectives as device plug-ins (the reference's
+generic-scalar contract, pkg/README.md:70-87) and the GPU fitting module
+(the reference's fitting.py) built on them.
+
+CPU tests: dataset handling / validation (no device needed).  GPU tests:
+NVRTC compile + value kernel vs numpy, zeus_run on a plug-in that restates a
+registered objective (same PSO swarm bit for bit, same statuses, minimisers
+within the stated tolerance), DomainError -> domain_error, compile errors,
+the chi^2 spectrum fit recovering the generating parameters, CLI `fit`."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import assert_outcomes_close
+from paper_2603_28770_b200 import cli, fitting
+
+RASTRIGIN_SRC = """
+template <class T, class X>
+__device__ T objective(const X& x, int d, const double* data, bool& err) {
+  T total = 10.0 * d;  // objectives.py:48-61, reference order
+  for (int i = 0; i < d; ++i) total = total + (x(i) * x(i) - 10.0 * zu::cos(zeus::two_pi() * x(i)));
+  return total;
+}
+"""
+
+WAVY_SRC = """
+template <class T, class X>
+__device__ T objective(const X& x, int d, const double* data, bool& err) {
+  T total = 0.0;
+  for (int i = 0; i < d; ++i) total = total + data[i] * x(i) * x(i) - zu::cos(3.0 * x(i));
+  return total;
+}
+"""
+
+
+# ---- CPU: datasets -----------------------------------------------------------
+def test_dataset_validation_and_io(tmp_path):
+    d = fitting.BinnedDataset(bin_edges=[0, 1, 2, 4], counts=[0, 4, 9])
+    assert np.array_equal(d.sigma, [1.0, 2.0, 3.0]) and d.n_bins == 3
+    assert np.array_equal(d.centers, [0.5, 1.5, 3.0])
+    for bad in (dict(bin_edges=[0, 1], counts=[1, 2]), dict(bin_edges=[0, 2, 1], counts=[1, 2]),
+                dict(bin_edges=[0, 1, 2], counts=[1, -1]),
+                dict(bin_edges=[0, 1, 2], counts=[1, 1], sigma=[1, 0])):
+        with pytest.raises(ValueError):
+            fitting.BinnedDataset(**bad)
+    p = tmp_path / "d.txt"
+    fitting.save_dataset(d, p)
+    back = fitting.load_dataset(p)
+    assert np.array_equal(back.bin_edges, d.bin_edges) and np.array_equal(back.sigma, d.sigma)
+    p.write_text("# comment\n0, 1, 5\n1 2 6 # trailing\n\n2 3 7\n")
+    assert np.array_equal(fitting.load_dataset(p).counts, [5, 6, 7])
+    p.write_text("0 1 5\n1.5 2 6\n")
+    with pytest.raises(ValueError, match="contiguous"):
+        fitting.load_dataset(p)
+    p.write_text("0 1 5\n1 2\n")
+    with pytest.raises(ValueError, match="columns"):
+        fitting.load_dataset(p)
+
+
+def test_falling_spectrum_host_model():
+    m = fitting.falling_spectrum(6000.0)
+    v = m.predict((50.0, 10.0, 5.0), 3000.0)
+    assert v == pytest.approx(50.0 * 0.5 ** 10 * 0.5 ** -5)
+    with pytest.raises(Exception):
+        m.predict((50.0, 10.0, 5.0), 7000.0)
+
+
+# ---- GPU --------------------------------------------------------------------
+@pytest.mark.gpu
+def test_plugin_values_and_data(z):
+    coef = [1.0, 2.0, 0.5]
+    f = z.DeviceObjective(WAVY_SRC, dim=3, data=coef, name="wavy")
+    pts = np.random.default_rng(0).uniform(-2, 2, size=(500, 3))
+    want = np.sum(np.array(coef) * pts * pts - np.cos(3.0 * pts), axis=1)
+    got = f.values(pts)
+    assert np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want))
+    assert f([0.0, 0.0, 0.0]) == -3.0
+
+
+@pytest.mark.gpu
+def test_plugin_matches_registered_objective(z):
+    """A plug-in restating Rastrigin: identical PSO swarm (same kernels, same
+    op order), identical statuses, minimisers within the stated tolerance."""
+    f = z.DeviceObjective(RASTRIGIN_SRC, dim=6, name="rastrigin_plugin")
+    cfg = z.ZeusConfig(N=2048, dim=6, range=(-5.12, 5.12), iter_pso=5, iter_bfgs=2000, seed=3,
+                       deterministic=True)
+    a = z.zeus_run(f, cfg)
+    b = z.zeus_run(z.rastrigin, cfg)
+    assert a.pso_best_before_bfgs == b.pso_best_before_bfgs
+    pa, pb = a.per_run, b.per_run
+    assert_outcomes_close(pa.x_final, pa.f_final, pa.status_codes, pb.x_final, pb.f_final,
+                          pb.status_codes, "plugin vs registered", pb.grad_norm)
+    pts = np.random.default_rng(1).uniform(-5, 5, size=(64, 6))
+    assert np.array_equal(f.values(pts),
+                          np.array([z.rastrigin(list(p)) for p in pts]))
+
+
+@pytest.mark.gpu
+def test_plugin_domain_error_and_compile_error(z):
+    src = """
+template <class T, class X>
+__device__ T objective(const X& x, int d, const double* data, bool& err) {
+  return zu::sqrt(x(0) * x(0) + x(1) * x(1), err);   // Ackley-like kink at 0
+}"""
+    f = z.DeviceObjective(src, dim=2, name="cone")
+    out = z.bfgs_run(f, [0.0, 0.0], theta=1e-6, iter_bfgs=50)
+    assert out.status == z.DOMAIN_ERROR and out.iterations == 0 and out.grad_norm == math.inf
+    out = z.bfgs_run(f, [1.0, 1.0], theta=1e-6, iter_bfgs=50)
+    assert out.status in (z.DOMAIN_ERROR, z.DIVERGED, z.CONVERGED)
+    with pytest.raises(ValueError, match="does not compile"):
+        z.DeviceObjective("this is not C++", dim=2)
+    with pytest.raises(ValueError):
+        z.DeviceObjective(src, dim=17)
+    with pytest.raises(NotImplementedError):
+        z.forward_gradient(f, [1.0, 2.0])
+
+
+@pytest.mark.gpu
+def test_spectrum_fit_recovers_parameters():
+    model = fitting.falling_spectrum(scale=6000.0)
+    edges = np.linspace(1200.0, 4800.0, 41)
+    truth = (50.0, 10.0, 5.0)
+    data = fitting.generate_spectrum_data(model, truth, edges)  # noiseless
+    out = fitting.fit(model, data, [1, 0, 0], [1000, 20, 10], seed=0)
+    assert out.chi_square < 1e-6
+    assert np.allclose(out.theta, truth, rtol=1e-3)
+    assert np.max(np.abs(out.pulls)) < 1e-3
+
+
+@pytest.mark.gpu
+def test_cli_fit_demo(tmp_path, capsys):
+    rep = tmp_path / "fit.txt"
+    assert cli.main(["fit", "--demo", "--report", str(rep)]) == cli.EXIT_OK
+    text = rep.read_text()
+    assert text.startswith("model: falling_spectrum\nbins: 40\n") and "chi_square:" in text
+    assert "of pulls within +-2" in capsys.readouterr().out

@@ -48,6 +48,9 @@ constexpr int kWideLd = 64;      // row stride of the shared-memory H rows
 #define ZEUS_WIDE_CH 4
 #endif
 constexpr int kCH = ZEUS_WIDE_CH;  // trials evaluated together (independent chains)
+#ifndef ZEUS_WIDE_SEQ
+#define ZEUS_WIDE_SEQ 1
+#endif
 #ifndef ZEUS_WIDE_UFROMP
 #define ZEUS_WIDE_UFROMP 1
 #endif
@@ -271,6 +274,60 @@ struct WideStart {
       neighbours(p0, p1, np0, np1);
       double alpha = 0.0, f_new = 0.0, acc_new[NA];
       int t_acc = -1;
+#if ZEUS_WIDE_SEQ
+      {
+        // chunks of kCH trials t0 .. t0 + kCH - 1 evaluated together, in order,
+        // until one passes: one copy of the chunk code (instruction cache) and
+        // no trial past the accepted chunk is evaluated
+        static_assert(kCH * NA <= 8, "one warp_sum8 per chunk");
+        for (int t0 = 0;; t0 += kCH) {
+          double al[kCH], sc[kCH][NA];
+#pragma unroll
+          for (int c = 0; c < kCH; ++c) al[c] = alpha_at(A, t0 + c);
+          bool oor = false;
+          lane_terms<FastMath, kCH>(d, nt, l, al, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
+          if (__any_sync(kFull, oor))  // some |2 pi x| > kTrigMax: CUDA libm, out of line
+            lane_terms_precise(d, nt, l, al, x0, x1, p0, p1, nx0, nx1, np0, np1, &sc[0][0]);
+          double v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = q < kCH * NA ? sc[q % kCH][q / kCH] : 0.0;
+          warp_sum8(v);
+          unsigned pm = 0u;
+          double fb[kCH];
+#pragma unroll
+          for (int c = 0; c < kCH; ++c) {
+            double ab[NA];
+#pragma unroll
+            for (int a = 0; a < NA; ++a) ab[a] = Obj::init(a, d) + v[a * kCH + c];
+            const bool valid = t0 + c <= A.iter_ls;
+            bool ferr = false;
+            if constexpr (NA > 1) {  // Ackley: exp / sqrt only for trials that exist
+              fb[c] = 0.0;
+              if (valid) fb[c] = Obj::finish(ab, d, ferr);
+            } else {
+              fb[c] = Obj::finish(ab, d, ferr);
+            }
+            // NaN fails; the trial at t = iter_ls is taken when nothing passed
+            const bool pass = fb[c] <= f0 + A.c1 * al[c] * ddir || t0 + c == A.iter_ls;
+            pm |= (valid && pass) ? (1u << c) : 0u;
+          }
+          if (pm) {
+            const int src = __ffs(pm) - 1;
+#pragma unroll
+            for (int c = 0; c < kCH; ++c) {
+              if (c == src) {
+                f_new = fb[c];
+                alpha = al[c];
+#pragma unroll
+                for (int a = 0; a < NA; ++a) acc_new[a] = Obj::init(a, d) + v[a * kCH + c];
+              }
+            }
+            t_acc = t0 + src;
+            break;
+          }
+        }
+      }
+#else
       {
         int t0 = 0;
         int B = min(max(prev_trials, 1), kWideMaxB);
@@ -341,6 +398,7 @@ struct WideStart {
           B = min(2 * B, kWideMaxB);
         }
       }
+#endif
       ls_trials += t_acc + 1;
       prev_trials = t_acc + 1;
 

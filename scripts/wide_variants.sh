@@ -14,7 +14,7 @@ while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   ( mkdir -p /tmp/wv_$name
     nvcc $FL $flags -c $C/bfgs_wide.cu -o /tmp/wv_$name/bfgs_wide.o 2> /tmp/wv_$name/ptxas.log
-    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o variants/lib_$name.so /tmp/wv_$name/bfgs_wide.o $OTHERS -lcudart
+    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o variants/lib_$name.so /tmp/wv_$name/bfgs_wide.o $OTHERS -lcudart -lnvrtc
     echo "$name: $(grep -A2 'bfgs_wide_kernel' /tmp/wv_$name/ptxas.log | grep -o 'Used [0-9]* registers\|[0-9]* bytes spill stores' | tr '\n' ' ')" ) &
   pids+=($!)
 done

@@ -106,9 +106,7 @@ struct BfgsWarp {
 #pragma unroll
         for (int a = 0; a < Obj::NACC; ++a) {
           const double* row = T + (a * A.bmax + lane) * A.tstride;
-          double sacc = Obj::init(a, d);
-          for (int j = 0; j < nt; ++j) sacc = sacc + row[j];
-          acc[a] = sacc;
+          acc[a] = seq_fold<DR>(row, nt, Obj::init(a, d));
         }
         bool err = false;
         f = Obj::finish(acc, d, err);

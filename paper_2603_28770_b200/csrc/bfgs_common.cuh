@@ -169,10 +169,27 @@ __device__ __forceinline__ void term_pass(int B, int nt, int total, const double
   }
 }
 
+// Reference-order fold s + row[0] + row[1] + ... of nt <= MAXT terms with
+// every load issued before the add chain (MAXT == 0: runtime loop).
+template <int MAXT>
+__device__ __forceinline__ double seq_fold(const double* row, int nt, double s) {
+  if constexpr (MAXT > 0) {
+    double v[MAXT];
+#pragma unroll
+    for (int j = 0; j < MAXT; ++j) v[j] = j < nt ? row[j] : 0.0;
+#pragma unroll
+    for (int j = 0; j < MAXT; ++j)
+      if (j < nt) s = s + v[j];
+  } else {
+    for (int j = 0; j < nt; ++j) s = s + row[j];
+  }
+  return s;
+}
+
 // Evaluate B trial points x + alpha_of[b] p (values AND term tangents);
 // lane b < B returns trial b's value and accumulators (reference-order fold).
 // B == 0 evaluates x itself.
-template <class Obj>
+template <class Obj, int MAXT = 0>
 __device__ __forceinline__ double eval_batch(int B, const double* alpha_of, int d,
                                              const double* x, const double* p, double* T,
                                              double* TT, int tstride, int rows, int lane,
@@ -193,9 +210,7 @@ __device__ __forceinline__ double eval_batch(int B, const double* alpha_of, int 
 #pragma unroll
     for (int a = 0; a < Obj::NACC; ++a) {
       const double* row = T + (a * rows + lane) * tstride;
-      double s = Obj::init(a, d);
-      for (int j = 0; j < nt; ++j) s = s + row[j];
-      acc[a] = s;
+      acc[a] = seq_fold<MAXT>(row, nt, Obj::init(a, d));
     }
     bool err = false;
     f = Obj::finish(acc, d, err);

@@ -44,10 +44,14 @@ namespace {
 constexpr int kWideWarps = 2;    // warps (starts) per block
 constexpr int kWideMaxB = 8;     // trials per speculative batch (registers)
 constexpr int kWideLd = 64;      // row stride of the shared-memory H rows
-#ifndef ZEUS_WIDE_CH
-#define ZEUS_WIDE_CH 4
+#ifdef ZEUS_WIDE_CH
+constexpr int kCH = ZEUS_WIDE_CH;  // trials per chunk of the batched (SEQ=0) search
+#else
+constexpr int kCH = 4;
 #endif
-constexpr int kCH = ZEUS_WIDE_CH;  // trials evaluated together (independent chains)
+#ifndef ZEUS_WIDE_ACKLEY
+#define ZEUS_WIDE_ACKLEY 1
+#endif
 #ifndef ZEUS_WIDE_SEQ
 #define ZEUS_WIDE_SEQ 1
 #endif
@@ -85,6 +89,20 @@ struct WideTraits {
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(kFull, v, src); }
 
 }  // namespace
+
+// Per-objective shape, tuned on B200 (scripts/wide_variants.sh +
+// scripts/phase_probe.py at d = 50): rows of H kept in registers (RR),
+// resident starts per SM (2 * MINB warps) and trials per line-search chunk
+// (CH: Ackley needs 1.6 trials per iteration, Rosenbrock 2.7, Rastrigin 6.2;
+// SM-cycles per start-iteration for CH = 1 / 2 / 3 / 4: Rosenbrock 820 / 770
+// / 781 / 793, Rastrigin 1781 / 1729 / 1746 / 1915, Ackley 1596 / 1854 (team
+// kernel: 2884)).
+template <class Obj>
+struct WideShape {
+  static constexpr int RR = Obj::kId == ZEUS_OBJ_ROSENBROCK ? 32 : 16;
+  static constexpr int MINB = Obj::kId == ZEUS_OBJ_ROSENBROCK ? 4 : 5;
+  static constexpr int CH = Obj::kId == ZEUS_OBJ_ACKLEY ? 1 : 2;
+};
 
 template <class Obj, int RR>
 struct WideStart {
@@ -131,15 +149,16 @@ struct WideStart {
 
   // Cold path: the chunk with CUDA libm trig (some argument beyond kTrigMax),
   // kept out of line so the hot loop stays small in the instruction cache.
+  template <int CH>
   __device__ __noinline__ void lane_terms_precise(int d, int nt, int l, const double* al,
                                                   double x0, double x1, double p0, double p1,
                                                   double nx0, double nx1, double np0,
                                                   double np1, double* out) const {
-    double a4[kCH], sc[kCH][NA];
-    for (int c = 0; c < kCH; ++c) a4[c] = al[c];
+    double a4[CH], sc[CH][NA];
+    for (int c = 0; c < CH; ++c) a4[c] = al[c];
     bool oor = false;
-    lane_terms<PreciseMath, kCH>(d, nt, l, a4, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
-    for (int c = 0; c < kCH; ++c)
+    lane_terms<PreciseMath, CH>(d, nt, l, a4, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
+    for (int c = 0; c < CH; ++c)
       for (int a = 0; a < NA; ++a) out[c * NA + a] = sc[c][a];
   }
 
@@ -276,29 +295,34 @@ struct WideStart {
       int t_acc = -1;
 #if ZEUS_WIDE_SEQ
       {
-        // chunks of kCH trials t0 .. t0 + kCH - 1 evaluated together, in order,
+#ifdef ZEUS_WIDE_CH
+        constexpr int CHK = ZEUS_WIDE_CH;
+#else
+        constexpr int CHK = WideShape<Obj>::CH;
+#endif
+        // chunks of CHK trials t0 .. t0 + CHK - 1 evaluated together, in order,
         // until one passes: one copy of the chunk code (instruction cache) and
         // no trial past the accepted chunk is evaluated
-        static_assert(kCH * NA <= 8, "one warp_sum8 per chunk");
-        for (int t0 = 0;; t0 += kCH) {
-          double al[kCH], sc[kCH][NA];
+        static_assert(CHK * NA <= 8, "one warp_sum8 per chunk");
+        for (int t0 = 0;; t0 += CHK) {
+          double al[CHK], sc[CHK][NA];
 #pragma unroll
-          for (int c = 0; c < kCH; ++c) al[c] = alpha_at(A, t0 + c);
+          for (int c = 0; c < CHK; ++c) al[c] = alpha_at(A, t0 + c);
           bool oor = false;
-          lane_terms<FastMath, kCH>(d, nt, l, al, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
+          lane_terms<FastMath, CHK>(d, nt, l, al, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
           if (__any_sync(kFull, oor))  // some |2 pi x| > kTrigMax: CUDA libm, out of line
-            lane_terms_precise(d, nt, l, al, x0, x1, p0, p1, nx0, nx1, np0, np1, &sc[0][0]);
+            lane_terms_precise<CHK>(d, nt, l, al, x0, x1, p0, p1, nx0, nx1, np0, np1, &sc[0][0]);
           double v[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v[q] = q < kCH * NA ? sc[q % kCH][q / kCH] : 0.0;
+          for (int q = 0; q < 8; ++q) v[q] = q < CHK * NA ? sc[q % CHK][q / CHK] : 0.0;
           warp_sum8(v);
           unsigned pm = 0u;
-          double fb[kCH];
+          double fb[CHK];
 #pragma unroll
-          for (int c = 0; c < kCH; ++c) {
+          for (int c = 0; c < CHK; ++c) {
             double ab[NA];
 #pragma unroll
-            for (int a = 0; a < NA; ++a) ab[a] = Obj::init(a, d) + v[a * kCH + c];
+            for (int a = 0; a < NA; ++a) ab[a] = Obj::init(a, d) + v[a * CHK + c];
             const bool valid = t0 + c <= A.iter_ls;
             bool ferr = false;
             if constexpr (NA > 1) {  // Ackley: exp / sqrt only for trials that exist
@@ -314,12 +338,12 @@ struct WideStart {
           if (pm) {
             const int src = __ffs(pm) - 1;
 #pragma unroll
-            for (int c = 0; c < kCH; ++c) {
+            for (int c = 0; c < CHK; ++c) {
               if (c == src) {
                 f_new = fb[c];
                 alpha = al[c];
 #pragma unroll
-                for (int a = 0; a < NA; ++a) acc_new[a] = Obj::init(a, d) + v[a * kCH + c];
+                for (int a = 0; a < NA; ++a) acc_new[a] = Obj::init(a, d) + v[a * CHK + c];
               }
             }
             t_acc = t0 + src;
@@ -351,7 +375,7 @@ struct WideStart {
               lane_terms<FastMath, kCH>(d, nt, l, al + c0, x0, x1, p0, p1, nx0, nx1, np0, np1,
                                         sc, oor);
               if (__any_sync(kFull, oor))  // some |2 pi x| > kTrigMax: CUDA libm, out of line
-                lane_terms_precise(d, nt, l, al + c0, x0, x1, p0, p1, nx0, nx1, np0, np1, &sc[0][0]);
+                lane_terms_precise<kCH>(d, nt, l, al + c0, x0, x1, p0, p1, nx0, nx1, np0, np1, &sc[0][0]);
 #pragma unroll
               for (int c = 0; c < kCH; ++c)
 #pragma unroll
@@ -596,19 +620,6 @@ struct WideStart {
 #define ZEUS_WIDE_MINB 5
 #endif
 
-// Per-objective shape, tuned on B200 (scripts/wide_variants.sh +
-// scripts/phase_probe.py at d = 50): rows of H kept in registers (RR) vs
-// resident starts per SM (2 * MINB warps).  Rosenbrock's cheap terms leave
-// registers for 32 H rows at 8 warps/SM; Rastrigin's trig chains want 10
-// warps/SM and 16 register rows.  (Ackley runs on the team kernel, which is
-// faster for it: its exp/sqrt finish and sincos gradient sit on the critical
-// path of a single warp.)
-template <class Obj>
-struct WideShape {
-  static constexpr int RR = Obj::kId == ZEUS_OBJ_ROSENBROCK ? 32 : 16;
-  static constexpr int MINB = Obj::kId == ZEUS_OBJ_ROSENBROCK ? 4 : 5;
-};
-
 #ifdef ZEUS_WIDE_RR_OVERRIDE
 #define ZEUS_WIDE_RR_OF(Obj) ZEUS_WIDE_RR_OVERRIDE
 #define ZEUS_WIDE_MINB_OF(Obj) ZEUS_WIDE_MINB
@@ -673,7 +684,8 @@ int launch_wide_rr(BfgsArgs A, cudaStream_t s) {
 struct WideLaunch {
   template <class Obj>
   static int run(BfgsArgs A, cudaStream_t s) {
-    if constexpr (Obj::kId == ZEUS_OBJ_GOLDSTEIN_PRICE || Obj::kId == ZEUS_OBJ_ACKLEY) {
+    if constexpr (Obj::kId == ZEUS_OBJ_GOLDSTEIN_PRICE ||
+                  (Obj::kId == ZEUS_OBJ_ACKLEY && !ZEUS_WIDE_ACKLEY)) {
       return set_error(ZEUS_ERR_UNSUPPORTED, "wide: objective runs on another kernel");
     } else {
       return launch_wide_rr<Obj, ZEUS_WIDE_RR_OF(Obj)>(A, s);
@@ -684,7 +696,9 @@ struct WideLaunch {
 }  // namespace
 
 bool bfgs_wide_covers(int obj, int d) {
-  return (obj == ZEUS_OBJ_ROSENBROCK || obj == ZEUS_OBJ_RASTRIGIN) && d > 32 && d <= 64;
+  return (obj == ZEUS_OBJ_ROSENBROCK || obj == ZEUS_OBJ_RASTRIGIN ||
+          (ZEUS_WIDE_ACKLEY && obj == ZEUS_OBJ_ACKLEY)) &&
+         d > 32 && d <= 64;
 }
 
 int launch_bfgs_wide(int obj, BfgsArgs A, cudaStream_t s) {

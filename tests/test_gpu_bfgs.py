@@ -78,7 +78,8 @@ def test_matches_oracle(oracle, name, d, n, cap):
 
 
 @pytest.mark.parametrize("name,d,n", [("rosenbrock", 50, 64), ("rastrigin", 50, 128),
-                                       ("rosenbrock", 37, 64), ("rastrigin", 61, 64)])
+                                       ("ackley", 50, 128), ("rosenbrock", 37, 64),
+                                       ("rastrigin", 61, 64), ("ackley", 33, 64)])
 def test_wide_kernel_matches_team_kernel(oracle, monkeypatch, name, d, n):
     """The warp-per-start (bfgs_wide.cu) and CTA-per-start (bfgs_team.cu)
     kernels implement the same iteration: identical statuses, minimisers

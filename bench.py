@@ -39,7 +39,8 @@ CONFIGS = {
     # north-star targets: 1,048,576 starts on 8 GPUs = 131,072 per GPU
     "t50r": ("rastrigin", 50, 131072, 5, 2000, (-5.12, 5.12)),
     "t50b": ("rosenbrock", 50, 131072, 5, 2000, (-5.0, 5.0)),
-    "c4": ("rosenbrock", 100, 8192, 5, 2000, (-5.0, 5.0)),
+    # BASELINE config 4: 1,048,576 starts over 8 GPUs = 131,072 per GPU
+    "c4": ("rosenbrock", 100, 131072, 5, 2000, (-5.0, 5.0)),
 }
 METRIC = "BFGS starts converged/sec"
 OBJ_IDS = {"rosenbrock": 0, "rastrigin": 1, "ackley": 2, "goldstein_price": 3}

@@ -1,60 +1,50 @@
-// bfgs_wide.cu -- multistart BFGS (bfgs.py:80-156) for 32 < d <= 64, one WARP
-// per start, built for throughput (the 1M-start 50-D targets).
+// bfgs_wide.cu -- multistart BFGS (bfgs.py:80-156) for 32 < d <= 128, one or
+// two WARPS per start, built for throughput (the 1M-start 50-D targets and
+// config 4's 100-D Rosenbrock).
 //
 // Why a second kernel family next to the CTA-per-start team kernel
 // (bfgs_team.cu): at d = 50 a team start costs ~7,300 cycles of wall time per
 // iteration, 55% of it in the CTA-synchronised line search and 24% in CTA
-// reductions, and only 4 starts fit an SM (scripts/phase_probe.py).  Here
-// everything is warp-synchronous (shuffles, no __syncthreads) and a start's
-// state is spread over the 32 lanes of one warp, so ~8-10 starts share an SM
-// and their latency-bound phases overlap each other's FP64 work.
+// reductions, and only 4 starts fit an SM (scripts/phase_probe.py).  Here a
+// start's state is spread over the lanes of W = 1 warp (d <= 64) or W = 2
+// warps (d <= 128); W = 1 is synchronised by shuffles only, W = 2 adds one
+// 64-thread barrier per reduction, so several starts share an SM and their
+// latency-bound phases overlap each other's FP64 work.
 //
-// Ownership: lane l owns coordinates c0 = l and c1 = l + 32 (if < d): their
-// x, p, g entries live in REGISTERS, and so do the first RR rows of the two
-// inverse-Hessian columns H[:, c0], H[:, c1]; rows RR..d-1 of those columns
-// live in the warp's shared-memory slice (conflict-free: lanes read
-// consecutive columns).  The per-row broadcast values of the fused H pass
-// {dg_i, g'_i, dx_i, u_i} are the only other shared-memory traffic.
+// Ownership: lane l of warp w owns coordinates c0 = 64 w + l and c1 = c0 + 32
+// (if < d): their x, p, g entries live in REGISTERS, and so do the first RR
+// rows of the two inverse-Hessian columns H[:, c0], H[:, c1]; rows RR..d-1 of
+// those columns live in the start's shared-memory slice (conflict-free: lanes
+// read consecutive columns).  The per-row broadcast values of the fused H
+// pass {dg_i, g'_i, dx_i, u_i} are the only other shared-memory traffic.
 //
 // Per iteration (reference order, bfgs.py:108-156):
-//  1. speculative batched Armijo search (linesearch.py:60-71): trials
-//     alpha0 shrink^t, t = t0..t0+B-1, evaluated together; every lane
-//     evaluates its own objective terms of every trial in registers
-//     (x + alpha p with the reference's two roundings), one transpose-reduce
-//     (warp_sum8) folds the B trials, and the FIRST passing trial is taken --
+//  1. Armijo search (linesearch.py:60-71) in chunks of CH trials
+//     alpha0 shrink^t evaluated together and tested in order until one passes:
+//     every lane evaluates its own objective terms of the chunk's trials in
+//     registers (x + alpha p with the reference's two roundings), one
+//     transpose-reduce folds them, and the FIRST passing trial is taken --
 //     alpha, trial count and f of the sequential search;
 //  2. gradient at x_new from lane-local forward-mode term tangents
 //     (autodiff.py:243-266 restricted to the terms that contain x_i; the one
 //     neighbour tangent Rosenbrock needs arrives by shuffle);
 //  3. one fused pass over H: the lazy rank-2 update of the previous iteration
-//     (H += dx a^T + u b^T, the O(d^2) form of bfgs.py:72-77), u = H dg and
-//     w = H g' in the same sweep;
-//  4. one 8-value warp reduction: |g'|^2, dx.dg, |dx|^2, |dg|^2, dg.u, u.g',
+//     (H += dx a^T + u b^T, the O(d^2) form of bfgs.py:72-77) and w = H g' in
+//     the same sweep; u = H dg = w + p (p = -H g is this iteration's
+//     direction), so one matvec per pass;
+//  4. one 8-value reduction: |g'|^2, dx.dg, |dx|^2, |dg|^2, dg.u, u.g',
 //     dx.g', w.g' -> curvature guard (bfgs.py:69-71), rho, the next direction
 //     p' = -H' g' = -(w - rho dx (u.g') - rho u (dx.g') + c dx (dx.g'));
 //  5. g'.p' (the next line search's ddir) by one butterfly.
-// Objective folds for d > 16 are warp trees (as in the team kernel): f agrees
-// with the reference's sequential fold to ~1 ulp, inside the stated tolerance.
+// Objective folds for d > 16 are trees (as in the team kernel): f agrees with
+// the reference's sequential fold to ~1 ulp, inside the stated tolerance.
 #include "bfgs_common.cuh"
 
 namespace zeus {
 
 namespace {
 
-constexpr int kWideWarps = 2;    // warps (starts) per block
-constexpr int kWideMaxB = 8;     // trials per speculative batch (registers)
-constexpr int kWideLd = 64;      // row stride of the shared-memory H rows
-#ifdef ZEUS_WIDE_CH
-constexpr int kCH = ZEUS_WIDE_CH;  // trials per chunk of the batched (SEQ=0) search
-#else
-constexpr int kCH = 4;
-#endif
-#ifndef ZEUS_WIDE_ACKLEY
-#define ZEUS_WIDE_ACKLEY 1
-#endif
-#ifndef ZEUS_WIDE_SEQ
-#define ZEUS_WIDE_SEQ 1
-#endif
+constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
 #ifndef ZEUS_WIDE_UFROMP
 #define ZEUS_WIDE_UFROMP 1
 #endif
@@ -92,24 +82,35 @@ __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(k
 
 // Per-objective shape, tuned on B200 (scripts/wide_variants.sh +
 // scripts/phase_probe.py at d = 50): rows of H kept in registers (RR),
-// resident starts per SM (2 * MINB warps) and trials per line-search chunk
-// (CH: Ackley needs 1.6 trials per iteration, Rosenbrock 2.7, Rastrigin 6.2;
-// SM-cycles per start-iteration for CH = 1 / 2 / 3 / 4: Rosenbrock 820 / 770
-// / 781 / 793, Rastrigin 1781 / 1729 / 1746 / 1915, Ackley 1596 / 1854 (team
-// kernel: 2884)).
-template <class Obj>
+// resident blocks per SM (MINB; 2 warps each) and trials per line-search
+// chunk (CH: Ackley needs 1.6 trials per iteration, Rosenbrock 2.7, Rastrigin
+// 6.2; SM-cycles per start-iteration for CH = 1 / 2 / 3 / 4: Rosenbrock 820 /
+// 770 / 781 / 793, Rastrigin 1781 / 1729 / 1746 / 1915, Ackley 1596 / 1854
+// (team kernel: 2884)).  W = 2 (64 < d <= 128) keeps 32 rows in registers.
+template <class Obj, int W>
 struct WideShape {
-  static constexpr int RR = Obj::kId == ZEUS_OBJ_ROSENBROCK ? 32 : 16;
-  static constexpr int MINB = Obj::kId == ZEUS_OBJ_ROSENBROCK ? 4 : 5;
+  static constexpr int RR = (W > 1 || Obj::kId == ZEUS_OBJ_ROSENBROCK) ? 32 : 16;
+  static constexpr int MINB = (W > 1 || Obj::kId == ZEUS_OBJ_ROSENBROCK) ? 4 : 5;
   static constexpr int CH = Obj::kId == ZEUS_OBJ_ACKLEY ? 1 : 2;
 };
 
-template <class Obj, int RR>
+// Shared-memory slice of one start, in doubles: rowv [64W][4], H rows
+// [d - RR][64W], exchange scratch (W > 1): two reduction buffers [2][W][8],
+// boundary values x, p, tangent [3][W].
+__host__ __device__ inline int wide_slot_doubles(int d, int rr, int w) {
+  return 4 * 64 * w + (d > rr ? d - rr : 0) * 64 * w + (w > 1 ? 16 * w + 3 * w : 0);
+}
+
+template <class Obj, int RR, int W>
 struct WideStart {
   static constexpr int NA = Obj::NACC;
-  double* Hs;          // [d - RR][kWideLd] rows RR.. of every column
-  double* rowv;        // [64][4] {dg, g', dx_prev, u_prev}
+  static constexpr int LD = 64 * W;  // row stride of the shared-memory H rows
+  double* Hs;          // [d - RR][LD] rows RR.. of every column of the start
+  double* rowv;        // [64 W][4] {dg, g', dx_prev, u_prev}
+  double* xch;         // W > 1: [2][W][8] reductions, then xb[W], pb[W], tb[W]
   const double* atab;  // block alpha table
+  int wi = 0;          // warp index within the start (0 .. W-1)
+  int slot = 0;        // reduction double-buffer
 
   __device__ __forceinline__ double alpha_at(const BfgsArgs& A, int t) const {
     if (t < A.nalpha) return atab[t];
@@ -118,16 +119,60 @@ struct WideStart {
     return a;
   }
 
+  // ---- team primitives (W == 1: the warp itself) -------------------------
+  __device__ __forceinline__ void team_sync() const {
+    if constexpr (W > 1) __syncthreads(); else __syncwarp();
+  }
+  __device__ __forceinline__ bool team_any(bool b) const {
+    if constexpr (W > 1) return __syncthreads_or(b); else return __any_sync(kFull, b);
+  }
+  // 8 values summed over the team, identical in every lane of every warp
+  // (warp transpose-reduce, then the W warp totals in warp order)
+  __device__ __forceinline__ void team_sum8(double v[8], int l) {
+    warp_sum8(v);
+    if constexpr (W > 1) {
+      double* r = xch + slot * 8 * W;
+      slot ^= 1;  // the next call's buffer: a warp cannot be two calls ahead
+      if (l == 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[wi * 8 + q] = v[q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double s = r[q];
+#pragma unroll
+        for (int w = 1; w < W; ++w) s += r[w * 8 + q];
+        v[q] = s;
+      }
+    }
+  }
+  __device__ __forceinline__ double team_sum(double v, int l) {
+    v = warp_sum(v);
+    if constexpr (W > 1) {
+      double* r = xch + slot * 8 * W;
+      slot ^= 1;
+      if (l == 0) r[wi * 8] = v;
+      __syncthreads();
+      double s = r[0];
+#pragma unroll
+      for (int w = 1; w < W; ++w) s += r[w * 8];
+      v = s;
+    }
+    return v;
+  }
+
   // Values of this lane's terms (c0, c1) at CH trial points x + alpha_c p,
   // s[c][a] = (0 + t(c0)) + t(c1) (the team kernel's lane order).  Branch-free:
   // all 2 CH term evaluations are independent chains the scheduler can
   // interleave (a missing term is evaluated at 0 and masked out).
   template <class M, int CH>
-  __device__ __forceinline__ void lane_terms(int d, int nt, int l, const double al[CH], double x0,
-                                             double x1, double p0, double p1, double nx0,
-                                             double nx1, double np0, double np1,
+  __device__ __forceinline__ void lane_terms(int d, int nt, int c0, const double al[CH],
+                                             double x0, double x1, double p0, double p1,
+                                             double nx0, double nx1, double np0, double np1,
                                              double s[CH][NA], bool& oor) const {
-    const bool v0 = l < nt, v1 = l + 32 < nt;
+    const int c1 = c0 + 32;
+    const bool v0 = c0 < nt, v1 = c1 < nt;
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const double xt0 = x0 + al[c] * p0, xt1 = x1 + al[c] * p1;
@@ -137,8 +182,8 @@ struct WideStart {
         xn1 = nx1 + al[c] * np1;
       }
       double t0[NA], t1[NA];
-      Obj::template term<M>(LX{l, xt0, xn0}, l, d, t0, oor);
-      Obj::template term<M>(LX{l + 32, xt1, xn1}, l + 32, d, t1, oor);
+      Obj::template term<M>(LX{c0, xt0, xn0}, c0, d, t0, oor);
+      Obj::template term<M>(LX{c1, xt1, xn1}, c1, d, t1, oor);
 #pragma unroll
       for (int a = 0; a < NA; ++a) {
         double v = v0 ? 0.0 + t0[a] : 0.0;
@@ -150,14 +195,14 @@ struct WideStart {
   // Cold path: the chunk with CUDA libm trig (some argument beyond kTrigMax),
   // kept out of line so the hot loop stays small in the instruction cache.
   template <int CH>
-  __device__ __noinline__ void lane_terms_precise(int d, int nt, int l, const double* al,
+  __device__ __noinline__ void lane_terms_precise(int d, int nt, int c0, const double* al,
                                                   double x0, double x1, double p0, double p1,
                                                   double nx0, double nx1, double np0,
                                                   double np1, double* out) const {
     double a4[CH], sc[CH][NA];
     for (int c = 0; c < CH; ++c) a4[c] = al[c];
     bool oor = false;
-    lane_terms<PreciseMath, CH>(d, nt, l, a4, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
+    lane_terms<PreciseMath, CH>(d, nt, c0, a4, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
     for (int c = 0; c < CH; ++c)
       for (int a = 0; a < NA; ++a) out[c * NA + a] = sc[c][a];
   }
@@ -165,13 +210,14 @@ struct WideStart {
   // Values AND term tangents of this lane's terms at the point (x0, x1)
   // (neighbour coordinates nx0, nx1); branch-free like lane_terms.
   template <class M>
-  __device__ __forceinline__ void lane_tan(int d, int nt, int l, double x0, double x1,
+  __device__ __forceinline__ void lane_tan(int d, int nt, int c0, double x0, double x1,
                                            double nx0, double nx1, double s[NA], double tA[2],
                                            double tB[2], bool& oor) const {
-    const bool v0 = l < nt, v1 = l + 32 < nt;
+    const int c1 = c0 + 32;
+    const bool v0 = c0 < nt, v1 = c1 < nt;
     double t0[NA], t1[NA], n0[Obj::KT], n1[Obj::KT];
-    Obj::template term_tan<M>(LX{l, x0, nx0}, l, d, t0, n0, oor);
-    Obj::template term_tan<M>(LX{l + 32, x1, nx1}, l + 32, d, t1, n1, oor);
+    Obj::template term_tan<M>(LX{c0, x0, nx0}, c0, d, t0, n0, oor);
+    Obj::template term_tan<M>(LX{c1, x1, nx1}, c1, d, t1, n1, oor);
 #pragma unroll
     for (int a = 0; a < NA; ++a) {
       double v = v0 ? 0.0 + t0[a] : 0.0;
@@ -184,40 +230,71 @@ struct WideStart {
   }
 
   // Gradient components of c0, c1 from the lane's term tangents (+ the
-  // neighbour's tangent of term c-1 w.r.t. x_c for Rosenbrock).
-  __device__ __forceinline__ void lane_grad(int d, int l, const double tA[2], const double tB[2],
-                                            const double acc[NA], double& g0, double& g1,
-                                            bool& err) const {
+  // neighbour's tangent of term c-1 w.r.t. x_c for Rosenbrock; across the
+  // warp boundary it comes through the exchange scratch).
+  __device__ __forceinline__ void lane_grad(int d, int l, int c0, const double tA[2],
+                                            const double tB[2], const double acc[NA],
+                                            double& g0, double& g1, bool& err) {
+    const int c1 = c0 + 32;
     double prevA = 0.0, prevB = 0.0;
     if constexpr (WideTraits<Obj>::kNeighbour) {
       const int src = (l + 31) & 31;
       const double s0 = shfl(tA[1], src), s1 = shfl(tB[1], src);
-      prevA = s0;                 // term l-1 (lane l-1's c0 term), l >= 1
-      prevB = l >= 1 ? s1 : s0;   // term l+31: lane l-1's c1 term, or lane 31's c0 term
+      prevA = s0;                 // term c0-1 (lane l-1's c0 term), l >= 1
+      prevB = l >= 1 ? s1 : s0;   // term c1-1: lane l-1's c1 term, or lane 31's c0 term
+      if constexpr (W > 1) {      // term 64w - 1: the previous warp's lane 31 c1 term
+        double* tb = xch + 16 * W + 2 * W;
+        if (l == 31) tb[wi] = tB[1];
+        __syncthreads();
+        if (l == 0 && wi > 0) prevA = tb[wi - 1];
+      }
     }
-    g0 = Obj::grad_from_tan(LT{l, tA[0], tA[1], prevA}, l, d, acc, err);
+    g0 = 0.0;
+    if (W == 1 || c0 < d) g0 = Obj::grad_from_tan(LT{c0, tA[0], tA[1], prevA}, c0, d, acc, err);
     g1 = 0.0;
-    if (l + 32 < d) g1 = Obj::grad_from_tan(LT{l + 32, tB[0], tB[1], prevB}, l + 32, d, acc, err);
+    if (c1 < d) g1 = Obj::grad_from_tan(LT{c1, tB[0], tB[1], prevB}, c1, d, acc, err);
   }
 
-  // f at a point from the lane sums s[a]: warp tree, then Obj::init + sum.
-  __device__ __forceinline__ double fold1(int d, const double s[NA], double acc[NA],
-                                          bool& err) const {
-#pragma unroll
-    for (int a = 0; a < NA; ++a) acc[a] = Obj::init(a, d) + warp_sum(s[a]);
-    return Obj::finish(acc, d, err);
+  // neighbour coordinates (Rosenbrock term j needs x_{j+1}) of two lane
+  // vectors (x and p); the last lane's c1 neighbour is the next warp's c0
+  __device__ __forceinline__ void neighbours2(int l, double x0, double x1, double p0, double p1,
+                                              double& nx0, double& nx1, double& np0,
+                                              double& np1) {
+    if constexpr (WideTraits<Obj>::kNeighbour) {
+      const int src = (l + 1) & 31;
+      const double tx0 = shfl(x0, src), tx1 = shfl(x1, src);
+      const double tp0 = shfl(p0, src), tp1 = shfl(p1, src);
+      nx0 = l < 31 ? tx0 : tx1;  // x_{c0+1}; lane 31 -> lane 0's c1
+      np0 = l < 31 ? tp0 : tp1;
+      nx1 = tx1;                 // x_{c1+1}; lane 31 -> next warp (below)
+      np1 = tp1;
+      if constexpr (W > 1) {
+        double* xb = xch + 16 * W;
+        double* pb = xb + W;
+        if (l == 0) {
+          xb[wi] = x0;
+          pb[wi] = p0;
+        }
+        __syncthreads();
+        if (l == 31) {
+          nx1 = wi + 1 < W ? xb[wi + 1] : 0.0;
+          np1 = wi + 1 < W ? pb[wi + 1] : 0.0;
+        }
+      }
+    }
   }
 
   __device__ void run(const BfgsArgs& A, long long s, int l) {
     const int d = A.d;
     const int nt = Obj::nterms(d);
-    const bool own1 = l + 32 < d;
+    const int c0 = 64 * wi + l, c1 = c0 + 32;
+    const bool own0 = W == 1 || c0 < d, own1 = c1 < d;
     double h0[RR], h1[RR];
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;  // pending rank-2 coefficients
-    double x0, x1 = 0.0, p0, p1 = 0.0, g0, g1 = 0.0;
+    double x0 = 0.0, x1 = 0.0, p0 = 0.0, p1 = 0.0, g0 = 0.0, g1 = 0.0;
     double acc[NA];
     double f0;
-    int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
+    int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0;
     double gnorm = __longlong_as_double(0x7ff0000000000000LL);
     double ddir = 0.0;
     bool pending = false;
@@ -225,55 +302,48 @@ struct WideStart {
     // ---- H = I, x = x0, rowv = 0
 #pragma unroll
     for (int i = 0; i < RR; ++i) {
-      h0[i] = i == l ? 1.0 : 0.0;
-      h1[i] = i == l + 32 ? 1.0 : 0.0;
+      h0[i] = i == c0 ? 1.0 : 0.0;
+      h1[i] = i == c1 ? 1.0 : 0.0;
     }
     for (int i = RR; i < d; ++i) {
-      Hs[(i - RR) * kWideLd + l] = i == l ? 1.0 : 0.0;
-      Hs[(i - RR) * kWideLd + l + 32] = i == l + 32 ? 1.0 : 0.0;
+      Hs[(i - RR) * LD + c0] = i == c0 ? 1.0 : 0.0;
+      Hs[(i - RR) * LD + c1] = i == c1 ? 1.0 : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      rowv[4 * l + q] = 0.0;
-      rowv[4 * (l + 32) + q] = 0.0;
+      rowv[4 * c0 + q] = 0.0;
+      rowv[4 * c1 + q] = 0.0;
     }
-    x0 = A.x0[(int64_t)l * A.ldx + s];
-    if (own1) x1 = A.x0[(int64_t)(l + 32) * A.ldx + s];
-    __syncwarp();
+    if (own0) x0 = A.x0[(int64_t)c0 * A.ldx + s];
+    if (own1) x1 = A.x0[(int64_t)c1 * A.ldx + s];
+    team_sync();
 
-    // neighbour coordinates of the current point (Rosenbrock term j needs x_{j+1})
-    double nx0 = 0.0, nx1 = 0.0;
-    auto neighbours = [&](double v0, double v1, double& n0, double& n1) {
-      if constexpr (WideTraits<Obj>::kNeighbour) {
-        const int src = (l + 1) & 31;
-        const double t0 = shfl(v0, src), t1 = shfl(v1, src);
-        n0 = l < 31 ? t0 : t1;  // x_{l+1}; lane 31 -> x_32 = lane 0's c1
-        n1 = t1;                // x_{l+33}
-      }
-    };
+    double nx0 = 0.0, nx1 = 0.0, np0 = 0.0, np1 = 0.0;
 
     // ---- f(x0) and the first gradient, from one term pass with tangents
     {
-      neighbours(x0, x1, nx0, nx1);
+      neighbours2(l, x0, x1, 0.0, 0.0, nx0, nx1, np0, np1);
       double sv[NA], tA[2], tB[2];
       bool oor = false, err = false;
-      lane_tan<FastMath>(d, nt, l, x0, x1, nx0, nx1, sv, tA, tB, oor);
-      if (__any_sync(kFull, oor)) lane_tan<PreciseMath>(d, nt, l, x0, x1, nx0, nx1, sv, tA, tB, oor);
+      lane_tan<FastMath>(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB, oor);
+      if (team_any(oor)) lane_tan<PreciseMath>(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB, oor);
+#pragma unroll
+      for (int a = 0; a < NA; ++a) acc[a] = Obj::init(a, d) + team_sum(sv[a], l);
       bool ferr = false;
-      f0 = fold1(d, sv, acc, ferr);
-      if (A.stop_flag && *(volatile int*)A.stop_flag) {
+      f0 = Obj::finish(acc, d, ferr);
+      if (A.stop_flag && team_any(*(volatile int*)A.stop_flag != 0)) {
         status = ZEUS_STOPPED;
         goto done;
       }
       ++grads;
-      lane_grad(d, l, tA, tB, acc, g0, g1, err);
-      if (__any_sync(kFull, err)) {
+      lane_grad(d, l, c0, tA, tB, acc, g0, g1, err);
+      if (team_any(err)) {
         status = ZEUS_DOMAIN_ERROR;
         goto done;
       }
       p0 = -g0;  // H0 = I: -(I @ g) is exact
       p1 = -g1;
-      const double gg = warp_sum(fma(g1, g1, g0 * g0));
+      const double gg = team_sum(fma(g1, g1, g0 * g0), l);
       gnorm = sqrt(gg);
       ddir = -gg;
     }
@@ -287,42 +357,38 @@ struct WideStart {
         status = ZEUS_DIVERGED;
         break;
       }
-      // ---- speculative batched Armijo search (linesearch.py:60-71)
-      double np0 = 0.0, np1 = 0.0;
-      neighbours(x0, x1, nx0, nx1);
-      neighbours(p0, p1, np0, np1);
+      // ---- Armijo search (linesearch.py:60-71): chunks of CH trials
+      // t0 .. t0 + CH - 1 evaluated together, in order, until one passes
+      neighbours2(l, x0, x1, p0, p1, nx0, nx1, np0, np1);
       double alpha = 0.0, f_new = 0.0, acc_new[NA];
       int t_acc = -1;
-#if ZEUS_WIDE_SEQ
       {
 #ifdef ZEUS_WIDE_CH
-        constexpr int CHK = ZEUS_WIDE_CH;
+        constexpr int CH = ZEUS_WIDE_CH;
 #else
-        constexpr int CHK = WideShape<Obj>::CH;
+        constexpr int CH = WideShape<Obj, W>::CH;
 #endif
-        // chunks of CHK trials t0 .. t0 + CHK - 1 evaluated together, in order,
-        // until one passes: one copy of the chunk code (instruction cache) and
-        // no trial past the accepted chunk is evaluated
-        static_assert(CHK * NA <= 8, "one warp_sum8 per chunk");
-        for (int t0 = 0;; t0 += CHK) {
-          double al[CHK], sc[CHK][NA];
+        static_assert(CH * NA <= 8, "one reduction per chunk");
+        for (int t0 = 0;; t0 += CH) {
+          double al[CH], sc[CH][NA];
 #pragma unroll
-          for (int c = 0; c < CHK; ++c) al[c] = alpha_at(A, t0 + c);
+          for (int c = 0; c < CH; ++c) al[c] = alpha_at(A, t0 + c);
           bool oor = false;
-          lane_terms<FastMath, CHK>(d, nt, l, al, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
-          if (__any_sync(kFull, oor))  // some |2 pi x| > kTrigMax: CUDA libm, out of line
-            lane_terms_precise<CHK>(d, nt, l, al, x0, x1, p0, p1, nx0, nx1, np0, np1, &sc[0][0]);
+          lane_terms<FastMath, CH>(d, nt, c0, al, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
+          if (team_any(oor))  // some |2 pi x| > kTrigMax: CUDA libm, out of line
+            lane_terms_precise<CH>(d, nt, c0, al, x0, x1, p0, p1, nx0, nx1, np0, np1,
+                                   &sc[0][0]);
           double v[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v[q] = q < CHK * NA ? sc[q % CHK][q / CHK] : 0.0;
-          warp_sum8(v);
+          for (int q = 0; q < 8; ++q) v[q] = q < CH * NA ? sc[q % CH][q / CH] : 0.0;
+          team_sum8(v, l);
           unsigned pm = 0u;
-          double fb[CHK];
+          double fb[CH];
 #pragma unroll
-          for (int c = 0; c < CHK; ++c) {
+          for (int c = 0; c < CH; ++c) {
             double ab[NA];
 #pragma unroll
-            for (int a = 0; a < NA; ++a) ab[a] = Obj::init(a, d) + v[a * CHK + c];
+            for (int a = 0; a < NA; ++a) ab[a] = Obj::init(a, d) + v[a * CH + c];
             const bool valid = t0 + c <= A.iter_ls;
             bool ferr = false;
             if constexpr (NA > 1) {  // Ackley: exp / sqrt only for trials that exist
@@ -338,12 +404,12 @@ struct WideStart {
           if (pm) {
             const int src = __ffs(pm) - 1;
 #pragma unroll
-            for (int c = 0; c < CHK; ++c) {
+            for (int c = 0; c < CH; ++c) {
               if (c == src) {
                 f_new = fb[c];
                 alpha = al[c];
 #pragma unroll
-                for (int a = 0; a < NA; ++a) acc_new[a] = Obj::init(a, d) + v[a * CHK + c];
+                for (int a = 0; a < NA; ++a) acc_new[a] = Obj::init(a, d) + v[a * CH + c];
               }
             }
             t_acc = t0 + src;
@@ -351,83 +417,10 @@ struct WideStart {
           }
         }
       }
-#else
-      {
-        int t0 = 0;
-        int B = min(max(prev_trials, 1), kWideMaxB);
-        for (;;) {
-          B = min(B, A.iter_ls + 1 - t0);
-          double al[8];  // the batch's step lengths, alpha0 shrink^(t0 + b)
-#pragma unroll
-          for (int b = 0; b < 8; ++b) al[b] = alpha_at(A, t0 + b);
-          double v[NA][8];
-#pragma unroll
-          for (int a = 0; a < NA; ++a)
-#pragma unroll
-            for (int b = 0; b < 8; ++b) v[a][b] = 0.0;
-          // trials in chunks of CH evaluated together (the last chunk may
-          // evaluate trials past B; they are never selected)
-#pragma unroll
-          for (int c0 = 0; c0 < 8; c0 += kCH) {
-            if (c0 < B) {
-              double sc[kCH][NA];
-              bool oor = false;
-              lane_terms<FastMath, kCH>(d, nt, l, al + c0, x0, x1, p0, p1, nx0, nx1, np0, np1,
-                                        sc, oor);
-              if (__any_sync(kFull, oor))  // some |2 pi x| > kTrigMax: CUDA libm, out of line
-                lane_terms_precise<kCH>(d, nt, l, al + c0, x0, x1, p0, p1, nx0, nx1, np0, np1, &sc[0][0]);
-#pragma unroll
-              for (int c = 0; c < kCH; ++c)
-#pragma unroll
-                for (int a = 0; a < NA; ++a) v[a][c0 + c] = sc[c][a];
-            }
-          }
-#pragma unroll
-          for (int a = 0; a < NA; ++a) warp_sum8(v[a]);
-          // Armijo test of every trial (identical in all lanes), then the
-          // FIRST passing one; the batch's last trial at t = iter_ls is taken
-          // when nothing passes (linesearch.py:71)
-          unsigned pm = 0u;
-          double fb[8];
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            double ab[NA];
-#pragma unroll
-            for (int a = 0; a < NA; ++a) ab[a] = Obj::init(a, d) + v[a][b];
-            bool ferr = false;
-            if constexpr (NA > 1) {  // Ackley: exp / sqrt only for evaluated trials
-              fb[b] = 0.0;
-              if (b < B) fb[b] = Obj::finish(ab, d, ferr);
-            } else {
-              fb[b] = Obj::finish(ab, d, ferr);
-            }
-            const bool pass = fb[b] <= f0 + A.c1 * al[b] * ddir || t0 + b >= A.iter_ls;
-            pm |= (b < B && pass) ? (1u << b) : 0u;
-          }
-          if (pm) {
-            const int src = __ffs(pm) - 1;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-              if (b == src) {
-                f_new = fb[b];
-                alpha = al[b];
-#pragma unroll
-                for (int a = 0; a < NA; ++a) acc_new[a] = Obj::init(a, d) + v[a][b];
-              }
-            }
-            t_acc = t0 + src;
-            break;
-          }
-          t0 += B;
-          B = min(2 * B, kWideMaxB);
-        }
-      }
-#endif
       ls_trials += t_acc + 1;
-      prev_trials = t_acc + 1;
 
       // ---- x_new and the gradient there (bfgs.py:136); DomainError leaves x, k
-      const double xn0 = x0 + alpha * p0;
+      const double xn0 = own0 ? x0 + alpha * p0 : 0.0;
       const double xn1 = own1 ? x1 + alpha * p1 : 0.0;
       ++grads;
       double gn0, gn1;
@@ -439,24 +432,21 @@ struct WideStart {
         }
         double sv[NA], tA[2], tB[2];
         bool oor = false, err = false;
-        lane_tan<FastMath>(d, nt, l, xn0, xn1, nxn0, nxn1, sv, tA, tB, oor);
-        if (__any_sync(kFull, oor))
-          lane_tan<PreciseMath>(d, nt, l, xn0, xn1, nxn0, nxn1, sv, tA, tB, oor);
-        lane_grad(d, l, tA, tB, acc_new, gn0, gn1, err);
-        if (__any_sync(kFull, err)) {
+        lane_tan<FastMath>(d, nt, c0, xn0, xn1, nxn0, nxn1, sv, tA, tB, oor);
+        if (team_any(oor))
+          lane_tan<PreciseMath>(d, nt, c0, xn0, xn1, nxn0, nxn1, sv, tA, tB, oor);
+        lane_grad(d, l, c0, tA, tB, acc_new, gn0, gn1, err);
+        if (team_any(err)) {
           status = ZEUS_DOMAIN_ERROR;
           break;
         }
       }
       const double dg0 = gn0 - g0, dg1 = gn1 - g1;
-      {
-        double2* r0 = reinterpret_cast<double2*>(rowv + 4 * l);
-        r0[0] = make_double2(dg0, gn0);
-        if (own1) reinterpret_cast<double2*>(rowv + 4 * (l + 32))[0] = make_double2(dg1, gn1);
-      }
-      __syncwarp();
+      if (own0) reinterpret_cast<double2*>(rowv + 4 * c0)[0] = make_double2(dg0, gn0);
+      if (own1) reinterpret_cast<double2*>(rowv + 4 * c1)[0] = make_double2(dg1, gn1);
+      team_sync();
 
-      // ---- fused pass over my two columns: lazy update, u = H dg, w = H g'
+      // ---- fused pass over my two columns: lazy update, w = H g' (u = w + p)
       double u0 = 0.0, w0 = 0.0, u1 = 0.0, w1 = 0.0;
       {
         double u0b = 0.0, w0b = 0.0, u1b = 0.0, w1b = 0.0;
@@ -488,17 +478,17 @@ struct WideStart {
           const double2 rb = *reinterpret_cast<const double2*>(rowv + 4 * i + 2);
           const double2 rc = *reinterpret_cast<const double2*>(rowv + 4 * i + 4);
           const double2 rd = *reinterpret_cast<const double2*>(rowv + 4 * i + 6);
-          double* hr = Hs + (i - RR) * kWideLd;
-          double e0 = hr[l], e1 = hr[l + 32], f0v = hr[kWideLd + l], f1v = hr[kWideLd + l + 32];
+          double* hr = Hs + (i - RR) * LD;
+          double e0 = hr[c0], e1 = hr[c1], f0v = hr[LD + c0], f1v = hr[LD + c1];
           if (pending) {
             e0 = fma(rb.x, a0, fma(rb.y, b0, e0));
             e1 = fma(rb.x, a1, fma(rb.y, b1, e1));
             f0v = fma(rd.x, a0, fma(rd.y, b0, f0v));
             f1v = fma(rd.x, a1, fma(rd.y, b1, f1v));
-            hr[l] = e0;
-            hr[l + 32] = e1;
-            hr[kWideLd + l] = f0v;
-            hr[kWideLd + l + 32] = f1v;
+            hr[c0] = e0;
+            hr[c1] = e1;
+            hr[LD + c0] = f0v;
+            hr[LD + c1] = f1v;
           }
           UACC(u0 = fma(e0, ra.x, u0));
           w0 = fma(e0, ra.y, w0);
@@ -512,13 +502,13 @@ struct WideStart {
         if (i < d) {
           const double2 ra = *reinterpret_cast<const double2*>(rowv + 4 * i);
           const double2 rb = *reinterpret_cast<const double2*>(rowv + 4 * i + 2);
-          double* hr = Hs + (i - RR) * kWideLd;
-          double e0 = hr[l], e1 = hr[l + 32];
+          double* hr = Hs + (i - RR) * LD;
+          double e0 = hr[c0], e1 = hr[c1];
           if (pending) {
             e0 = fma(rb.x, a0, fma(rb.y, b0, e0));
             e1 = fma(rb.x, a1, fma(rb.y, b1, e1));
-            hr[l] = e0;
-            hr[l + 32] = e1;
+            hr[c0] = e0;
+            hr[c1] = e1;
           }
           UACC(u0b = fma(e0, ra.x, u0b));
           w0b = fma(e0, ra.y, w0b);
@@ -538,10 +528,12 @@ struct WideStart {
         u0 += u0b;
         u1 += u1b;
 #endif
+        if (!own0) u0 = w0 = 0.0;
+        if (!own1) u1 = w1 = 0.0;
       }
 
       // ---- one 8-value reduction: norms, curvature and the p' scalars
-      const double dx0 = xn0 - x0, dx1 = own1 ? xn1 - x1 : 0.0;
+      const double dx0 = own0 ? xn0 - x0 : 0.0, dx1 = own1 ? xn1 - x1 : 0.0;
       double part[8];
       part[0] = fma(gn1, gn1, gn0 * gn0);
       part[1] = fma(dx1, dg1, dx0 * dg0);
@@ -551,11 +543,11 @@ struct WideStart {
       part[5] = fma(u1, gn1, u0 * gn0);
       part[6] = fma(dx1, gn1, dx0 * gn0);
       part[7] = fma(w1, gn1, w0 * gn0);
-      warp_sum8(part);
+      team_sum8(part, l);  // W > 1: its barrier also ends every read of rowv
       const double curv = part[1];
       const double ndx = sqrt(part[2]), ndg = sqrt(part[3]);
       pending = !(curv <= kCurvatureFloor * ndx * ndg);  // bfgs.py:69-71
-      __syncwarp();  // rowv (dx/u of the previous iteration) fully consumed
+      if constexpr (W == 1) __syncwarp();  // rowv (dx/u of the previous iteration) consumed
       double pd;
       {
         const double rho = pending ? 1.0 / curv : 0.0;
@@ -570,9 +562,10 @@ struct WideStart {
           b0 = -rho * dx0;
           a1 = fma(cc, dx1, -rho * u1);
           b1 = -rho * dx1;
-          reinterpret_cast<double2*>(rowv + 4 * l)[1] = make_double2(dx0, u0);
-          if (own1) reinterpret_cast<double2*>(rowv + 4 * (l + 32))[1] = make_double2(dx1, u1);
+          if (own0) reinterpret_cast<double2*>(rowv + 4 * c0)[1] = make_double2(dx0, u0);
+          if (own1) reinterpret_cast<double2*>(rowv + 4 * c1)[1] = make_double2(dx1, u1);
         }
+        if (!own0) q0 = 0.0;
         if (!own1) q1 = 0.0;
         p0 = q0;
         p1 = q1;
@@ -587,10 +580,10 @@ struct WideStart {
 #pragma unroll
       for (int a = 0; a < NA; ++a) acc[a] = acc_new[a];
       gnorm = sqrt(part[0]);
-      ddir = warp_sum(pd);  // np.dot(g, p) of the next line search
+      ddir = team_sum(pd, l);  // np.dot(g, p) of the next line search
       ++k;
-      __syncwarp();
-      if (A.stop_flag && *(volatile int*)A.stop_flag) {
+      if constexpr (W == 1) __syncwarp();
+      if (A.stop_flag && team_any(*(volatile int*)A.stop_flag != 0)) {
         status = ZEUS_STOPPED;
         break;
       }
@@ -598,9 +591,9 @@ struct WideStart {
 
   done:
     const zeus_bfgs_out& o = A.out;
-    o.x_final[(int64_t)l * o.ld_out + s] = x0;
-    if (own1) o.x_final[(int64_t)(l + 32) * o.ld_out + s] = x1;
-    if (l == 0) {
+    if (own0) o.x_final[(int64_t)c0 * o.ld_out + s] = x0;
+    if (own1) o.x_final[(int64_t)c1 * o.ld_out + s] = x1;
+    if (wi == 0 && l == 0) {
       o.f_final[s] = f0;
       o.grad_norm[s] = gnorm;
       o.iterations[s] = k;
@@ -612,24 +605,12 @@ struct WideStart {
         if ((long long)old + 1 == A.required_c) atomicExch_system(A.stop_flag, 1);
       }
     }
-    __syncwarp();
+    team_sync();
   }
 };
 
-#ifndef ZEUS_WIDE_MINB
-#define ZEUS_WIDE_MINB 5
-#endif
-
-#ifdef ZEUS_WIDE_RR_OVERRIDE
-#define ZEUS_WIDE_RR_OF(Obj) ZEUS_WIDE_RR_OVERRIDE
-#define ZEUS_WIDE_MINB_OF(Obj) ZEUS_WIDE_MINB
-#else
-#define ZEUS_WIDE_RR_OF(Obj) WideShape<Obj>::RR
-#define ZEUS_WIDE_MINB_OF(Obj) WideShape<Obj>::MINB
-#endif
-
-template <class Obj, int RR>
-__global__ void __launch_bounds__(kWideWarps * 32, ZEUS_WIDE_MINB_OF(Obj))
+template <class Obj, int RR, int W>
+__global__ void __launch_bounds__(kWideThreads, WideShape<Obj, W>::MINB)
     bfgs_wide_kernel(BfgsArgs A) {
   extern __shared__ double sm[];
   const int l = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -642,53 +623,71 @@ __global__ void __launch_bounds__(kWideWarps * 32, ZEUS_WIDE_MINB_OF(Obj))
     }
   }
   __syncthreads();
-  WideStart<Obj, RR> W;
-  W.atab = alpha_tab;
-  W.rowv = sm + A.nalpha + (size_t)wib * A.warp_doubles;
-  W.Hs = W.rowv + 4 * 64;
+  WideStart<Obj, RR, W> S;
+  const int start_slot = wib / W;  // W = 1: two independent starts per block
+  S.wi = wib % W;
+  S.atab = alpha_tab;
+  S.rowv = sm + A.nalpha + (size_t)start_slot * A.warp_doubles;
+  S.Hs = S.rowv + 4 * 64 * W;
+  S.xch = S.Hs + (size_t)(A.d > RR ? A.d - RR : 0) * 64 * W;
+  __shared__ long long next;
   for (;;) {
     long long s = 0;
-    if (l == 0) s = (long long)atomicAdd(A.work, 1ull);
-    s = __shfl_sync(kFull, s, 0);
+    if constexpr (W == 1) {
+      if (l == 0) s = (long long)atomicAdd(A.work, 1ull);
+      s = __shfl_sync(kFull, s, 0);
+    } else {
+      if (threadIdx.x == 0) next = (long long)atomicAdd(A.work, 1ull);
+      __syncthreads();
+      s = next;
+      __syncthreads();
+    }
     if (s >= A.n) break;
-    W.run(A, s, l);
+    S.run(A, s, l);
   }
 }
 
 namespace {
 
-template <class Obj, int RR>
-int launch_wide_rr(BfgsArgs A, cudaStream_t s) {
+template <class Obj, int RR, int W>
+int launch_wide(BfgsArgs A, cudaStream_t s) {
   A.nalpha = kAlphaTable;
-  A.warp_doubles = 4 * 64 + std::max(0, A.d - RR) * kWideLd;
-  const size_t smem = sizeof(double) * ((size_t)A.nalpha + (size_t)kWideWarps * A.warp_doubles);
-  auto kern = bfgs_wide_kernel<Obj, RR>;
+  A.warp_doubles = wide_slot_doubles(A.d, RR, W);  // per start
+  const int starts_per_block = 2 / W;
+  const size_t smem =
+      sizeof(double) * ((size_t)A.nalpha + (size_t)starts_per_block * A.warp_doubles);
+  auto kern = bfgs_wide_kernel<Obj, RR, W>;
   int rc = check_cuda(
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
       "cudaFuncSetAttribute(wide)");
   if (rc) return rc;
   int per_sm = 0;
-  rc = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWideWarps * 32, smem),
+  rc = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWideThreads, smem),
                   "occupancy(wide)");
   if (rc) return rc;
   const int sms = current_sm_count();
   if (per_sm < 1 || sms < 1) return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs wide: does not fit");
   int64_t grid = (int64_t)per_sm * sms;
-  const int64_t need = (A.n + kWideWarps - 1) / kWideWarps;
+  const int64_t need = (A.n + starts_per_block - 1) / starts_per_block;
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, kWideWarps * 32, smem, s>>>(A);
+  kern<<<(unsigned)grid, kWideThreads, smem, s>>>(A);
   return check_launch("bfgs_wide_kernel");
 }
 
+#ifdef ZEUS_WIDE_RR_OVERRIDE
+#define ZEUS_WIDE_RR_OF(Obj, W) ZEUS_WIDE_RR_OVERRIDE
+#else
+#define ZEUS_WIDE_RR_OF(Obj, W) WideShape<Obj, W>::RR
+#endif
 
 struct WideLaunch {
   template <class Obj>
   static int run(BfgsArgs A, cudaStream_t s) {
-    if constexpr (Obj::kId == ZEUS_OBJ_GOLDSTEIN_PRICE ||
-                  (Obj::kId == ZEUS_OBJ_ACKLEY && !ZEUS_WIDE_ACKLEY)) {
-      return set_error(ZEUS_ERR_UNSUPPORTED, "wide: objective runs on another kernel");
+    if constexpr (Obj::kId == ZEUS_OBJ_GOLDSTEIN_PRICE) {
+      return set_error(ZEUS_ERR_UNSUPPORTED, "wide: goldstein_price is 2-D");
     } else {
-      return launch_wide_rr<Obj, ZEUS_WIDE_RR_OF(Obj)>(A, s);
+      if (A.d <= 64) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1>(A, s);
+      return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2>(A, s);
     }
   }
 };
@@ -696,9 +695,7 @@ struct WideLaunch {
 }  // namespace
 
 bool bfgs_wide_covers(int obj, int d) {
-  return (obj == ZEUS_OBJ_ROSENBROCK || obj == ZEUS_OBJ_RASTRIGIN ||
-          (ZEUS_WIDE_ACKLEY && obj == ZEUS_OBJ_ACKLEY)) &&
-         d > 32 && d <= 64;
+  return obj != ZEUS_OBJ_GOLDSTEIN_PRICE && d > 32 && d <= 128;
 }
 
 int launch_bfgs_wide(int obj, BfgsArgs A, cudaStream_t s) {

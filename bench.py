@@ -311,11 +311,18 @@ def main():
                    "parallelism": f"start-sharded x{world}", "l2": "flushed between steps"},
         "time_to_solution_s": float(np.mean(dev_t)),
         "bfgs_ms_per_step": float(np.mean(bfgs_t)) * 1e3,
+        "pso_ms_per_step": float(np.mean(maxrank([r["pso"] for r in records]))) * 1e3,
         "bracket_ms_per_step": bracket / args.steps * 1e3,
         "converged_per_step": conv / args.steps,
         "e2e": {"value": conv / float(np.sum(wall_t)), "unit": "starts/s",
                 "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": int(records[0]["d2h"])},
+                "d2h_bytes_per_step": int(records[0]["d2h"]),
+                "path": "zeus_run(rastrigin, ZeusConfig(...)) wall time, per-start results "
+                        "(x_final, f, |g|, k, status, counters) copied to host every step",
+                "inputs": "the call's inputs are (objective, config, seed): kernel arguments "
+                          "only; the swarm is generated on the device from the seed by the "
+                          "reference's Philox stream (SURVEY S1), as the reference does on "
+                          "the host, so no input bytes cross PCIe"},
         "gpu_launches": int(sum(r["launches"] for r in records)),
         "roofline": {"bound": "fp64",
                      "kernel": "BFGS tiers of the step (bfgs_thread -> bfgs_warp -> CTA-team "

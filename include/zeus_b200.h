@@ -114,6 +114,16 @@ int zeus_pso_sweep(int obj, int d, int64_t n, int64_t i0, uint64_t seed, int swe
                    double w, double c1, double c2, double *x, double *v, double *pbest,
                    double *pval, int64_t ld, const double *gX, double *cand,
                    void *workspace, void *stream);
+/* The whole PSO phase when this shard is the whole swarm (one GPU): init_swarm
+ * + iter_pso update_swarm sweeps with the global-best barrier after each
+ * (pso.py:79-164, driver.py:236-241), 1 + iter_pso launches; the last block of
+ * every launch reduces the candidate and writes gX[d], gbest[2] = {f, index}
+ * (the barrier's result for the next sweep).  Same results as zeus_pso_init /
+ * zeus_pso_sweep + zeus_minloc_select(ncand = 1). */
+int zeus_pso_run(int obj, int d, int64_t n, int64_t i0, uint64_t seed, double lower,
+                 double upper, double w, double c1, double c2, int iter_pso, double *x,
+                 double *v, double *pbest, double *pval, int64_t ld, double *cand, double *gX,
+                 double *gbest, void *workspace, void *stream);
 /* _reduce_global_best across shards (pso.py:73-76): cands[ncand][d+2] from
  * every shard (e.g. an NCCL all-gather); writes the np.argmin winner to
  * gX[d] and gbest[2] = {f, (double)global_index}. */

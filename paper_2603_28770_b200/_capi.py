@@ -56,6 +56,8 @@ _SIGNATURES = {
     "zeus_pso_sweep": (_int, [_int, _int, _i64, _i64, _u64, _int, _dbl, _dbl, _dbl, _vp, _vp,
                               _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "zeus_minloc_select": (_int, [_int, _int, _vp, _vp, _vp, _vp]),
+    "zeus_pso_run": (_int, [_int, _int, _i64, _i64, _u64, _dbl, _dbl, _dbl, _dbl, _dbl, _int,
+                            _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "zeus_bfgs_workspace_bytes": (_sz, [_int, _i64]),
     "zeus_bfgs": (_int, [_int, _int, _i64, _vp, _i64, ctypes.POINTER(BfgsParams), _i64, _vp,
                          _vp, ctypes.POINTER(BfgsOut), _vp, _vp]),

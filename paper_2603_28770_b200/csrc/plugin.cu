@@ -236,8 +236,9 @@ int zeus_user_pso_init(void* handle, int64_t n, int64_t i0, uint64_t seed, doubl
   long long* blk_i = (long long*)(blk_f + nb);
   double range = upper - lower, vr = upper - lower;  // pso.py:101
   double vlow = -vr, vrange = vr - (-vr);
+  void* none = nullptr;
   void* args[] = {&d, &n, &i0, &seed, &lower, &range, &vlow, &vrange, &x, &v, &pbest, &pval,
-                  &ld, &blk_f, &blk_i};
+                  &ld, &blk_f, &blk_i, &none, &none, &none, &none};
   int rc = cu_check(drv().LaunchKernel(up->pso_init, nb, 1, 1, kPsoBlockU, 1, 1, 0, (CUstream)stream,
                                    args, nullptr),
                     "pso_init_kernel(user)");
@@ -258,8 +259,9 @@ int zeus_user_pso_sweep(void* handle, int64_t n, int64_t i0, uint64_t seed, int 
   double* blk_f = (double*)workspace;
   long long* blk_i = (long long*)(blk_f + nb);
   uint64_t k0 = (uint64_t)(2 * d) * (uint64_t)(sweep + 1);
+  void* none = nullptr;
   void* args[] = {&d, &n, &i0, &seed, &k0, &w, &c1, &c2, &x, &v, &pbest, &pval, &ld, &gX,
-                  &blk_f, &blk_i};
+                  &blk_f, &blk_i, &none, &none, &none, &none};
   int rc = cu_check(drv().LaunchKernel(up->pso_sweep, nb, 1, 1, kPsoBlockU, 1, 1, 0,
                                    (CUstream)stream, args, nullptr),
                     "pso_sweep_kernel(user)");

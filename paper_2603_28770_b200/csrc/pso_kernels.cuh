@@ -91,6 +91,69 @@ __device__ __forceinline__ StreamAcc<Obj> make_acc(int d) {
   else return StreamAcc<Obj>();
 }
 
+// Reduce block partials -> this shard's candidate [f, idx, pbest[:, idx]];
+// with gX / gbest (one shard: the candidate IS the global best, pso.py:73-76)
+// also the barrier's result.  Partials are read with __ldcg (written by
+// other SMs in the fused path).
+__device__ __forceinline__ void finalize_body(int d, int nb, int64_t i0,
+                                              const double* __restrict__ p, int64_t ld,
+                                              const double* blk_f, const long long* blk_i,
+                                              double* cand, double* gX, double* gbest) {
+  __shared__ long long win;
+  double bf = 0.0;
+  long long bi = -1;
+  for (int b = threadIdx.x; b < nb; b += kPsoBlock) {
+    const double fb = __ldcg(blk_f + b);
+    const long long ib = __ldcg(blk_i + b);
+    if (argmin_better(fb, ib, bf, bi)) {
+      bf = fb;
+      bi = ib;
+    }
+  }
+  block_argmin<kPsoBlock>(bf, bi);
+  if (threadIdx.x == 0) {
+    win = bi;
+    cand[0] = bf;
+    cand[1] = (double)bi;
+    if (gbest) {
+      gbest[0] = bf;
+      gbest[1] = (double)bi;
+    }
+  }
+  __syncthreads();
+  const long long li = win - i0;
+  for (int k = threadIdx.x; k < d; k += kPsoBlock) {
+    const double v = __ldcg(p + (int64_t)k * ld + li);
+    cand[2 + k] = v;
+    if (gX) gX[k] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kPsoBlock)
+    pso_finalize_kernel(int d, int nb, int64_t i0, const double* __restrict__ p, int64_t ld,
+                        const double* blk_f, const long long* blk_i, double* cand) {
+  finalize_body(d, nb, i0, p, ld, blk_f, blk_i, cand, nullptr, nullptr);
+}
+
+// Fused barrier (`done` != nullptr): the last block to finish reduces every
+// block's partial into the candidate (and, for one shard, the global best),
+// so a sweep is one launch.  Every block's writes are fenced before its ticket.
+__device__ __forceinline__ void fused_finalize(unsigned* done, int d, int64_t i0, const double* p,
+                                               int64_t ld, const double* blk_f,
+                                               const long long* blk_i, double* cand, double* gX,
+                                               double* gbest) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    finalize_body(d, (int)gridDim.x, i0, p, ld, blk_f, blk_i, cand, gX, gbest);
+    if (threadIdx.x == 0) *done = 0u;  // ready for the next launch
+  }
+}
+
 // init_swarm: positions U[lo,hi)^d from draws 0..d-1, velocities U[-vr,vr)^d
 // from draws d..2d-1 (pso.py:101-109); pbest = x; pval = f(x).
 template <class Obj>
@@ -98,7 +161,8 @@ __global__ void __launch_bounds__(kPsoBlock)
     pso_init_kernel(int d, int64_t n, int64_t i0, uint64_t seed, double lower, double range,
                     double vlow, double vrange, double* __restrict__ x, double* __restrict__ v,
                     double* __restrict__ p, double* __restrict__ pval, int64_t ld,
-                    double* blk_f, long long* blk_i) {
+                    double* blk_f, long long* blk_i, unsigned* done, double* cand,
+                    double* gX_out, double* gbest_out) {
   const int64_t i = blockIdx.x * (int64_t)kPsoBlock + threadIdx.x;
   double bf = 0.0;
   long long bi = -1;
@@ -123,6 +187,10 @@ __global__ void __launch_bounds__(kPsoBlock)
     blk_f[blockIdx.x] = bf;
     blk_i[blockIdx.x] = bi;
   }
+  if (done) {
+    __syncthreads();  // block_argmin's shared scratch is reused by the finalize
+    fused_finalize(done, d, i0, p, ld, blk_f, blk_i, cand, gX_out, gbest_out);
+  }
 }
 
 // update_swarm sweep s: r1 = draws 2d(s+1)+k, r2 = draws 2d(s+1)+d+k;
@@ -132,7 +200,8 @@ __global__ void __launch_bounds__(kPsoBlock)
     pso_sweep_kernel(int d, int64_t n, int64_t i0, uint64_t seed, uint64_t k0, double w,
                      double c1, double c2, double* __restrict__ x, double* __restrict__ v,
                      double* __restrict__ p, double* __restrict__ pval, int64_t ld,
-                     const double* __restrict__ gX, double* blk_f, long long* blk_i) {
+                     const double* gX, double* blk_f, long long* blk_i, unsigned* done,
+                     double* cand, double* gX_out, double* gbest_out) {
   const int64_t i = blockIdx.x * (int64_t)kPsoBlock + threadIdx.x;
   double bf = 0.0;
   long long bi = -1;
@@ -143,7 +212,7 @@ __global__ void __launch_bounds__(kPsoBlock)
       const double r1 = uniform_draw(c_r1.at(k0 + (uint64_t)k), 0.0, 1.0);
       const double r2 = uniform_draw(c_r2.at(k0 + (uint64_t)(d + k)), 0.0, 1.0);
       const int64_t o = (int64_t)k * ld + i;
-      const double xk = x[o], vk = v[o], pk = p[o], gk = __ldg(gX + k);
+      const double xk = x[o], vk = v[o], pk = p[o], gk = gX[k];
       const double nv = w * vk + c1 * r1 * (pk - xk) + c2 * r2 * (gk - xk);
       const double nx = xk + nv;
       v[o] = nv;
@@ -165,29 +234,10 @@ __global__ void __launch_bounds__(kPsoBlock)
     blk_f[blockIdx.x] = bf;
     blk_i[blockIdx.x] = bi;
   }
-}
-
-// Reduce block partials -> this shard's candidate [f, idx, pbest[:, idx]].
-__global__ void __launch_bounds__(kPsoBlock)
-    pso_finalize_kernel(int d, int nb, int64_t i0, const double* __restrict__ p, int64_t ld,
-                        const double* blk_f, const long long* blk_i, double* cand) {
-  __shared__ long long win;
-  double bf = 0.0;
-  long long bi = -1;
-  for (int b = threadIdx.x; b < nb; b += kPsoBlock)
-    if (argmin_better(blk_f[b], blk_i[b], bf, bi)) {
-      bf = blk_f[b];
-      bi = blk_i[b];
-    }
-  block_argmin<kPsoBlock>(bf, bi);
-  if (threadIdx.x == 0) {
-    win = bi;
-    cand[0] = bf;
-    cand[1] = (double)bi;
+  if (done) {
+    __syncthreads();  // block_argmin's shared scratch is reused by the finalize
+    fused_finalize(done, d, i0, p, ld, blk_f, blk_i, cand, gX_out, gbest_out);
   }
-  __syncthreads();
-  const long long li = win - i0;
-  for (int k = threadIdx.x; k < d; k += kPsoBlock) cand[2 + k] = p[(int64_t)k * ld + li];
 }
 
 }  // namespace zeus

@@ -268,18 +268,24 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
     pso_best = math.nan
     if starts is None:
         shard = engine.SwarmShard(obj, d, max(n, 1), lo, cfg.seed, dev)
-        barrier = engine.local_barrier if world == 1 else engine.make_dist_barrier(process_group)
         lower, upper = cfg.range
-        if n > 0:
-            shard.init(lower, upper)
+        if world == 1 and isinstance(obj, int):
+            # one GPU: the barrier is the shard's own candidate -> fused sweeps
+            shard.run_local(lower, upper, cfg.pso.w, cfg.pso.c1_pso, cfg.pso.c2_pso,
+                            cfg.iter_pso)
         else:
-            shard.cand.zero_()
-            shard.cand[1] = -1.0
-        barrier(shard)
-        for _ in range(cfg.iter_pso):
+            barrier = (engine.local_barrier if world == 1 else
+                       engine.make_dist_barrier(process_group))
             if n > 0:
-                shard.sweep(cfg.pso.w, cfg.pso.c1_pso, cfg.pso.c2_pso)
+                shard.init(lower, upper)
+            else:
+                shard.cand.zero_()
+                shard.cand[1] = -1.0
             barrier(shard)
+            for _ in range(cfg.iter_pso):
+                if n > 0:
+                    shard.sweep(cfg.pso.w, cfg.pso.c1_pso, cfg.pso.c2_pso)
+                barrier(shard)
         x0 = shard.x[:, :n]
         gbest = shard.gbest
     else:
@@ -340,7 +346,10 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
         engine.all_reduce_sum(tallies, group=process_group)
     ev_end.record(stream)
 
-    # ---- results to host (part of the end-to-end wall time)
+    # ---- results to host (part of the end-to-end wall time): the per-start
+    # columns are packed on the device into two row-major tables ([n][d + 2]
+    # f64: x, f, |g|; [n][4] i32: k, status, trials, gradients) and copied
+    # with one pinned, asynchronous D2H each; the host arrays are views
     per = -(-N // world)
     if world > 1 and gather:
         xs = _gather_rows(out.x_final[:, :n], per, world, process_group)[:, :N]
@@ -353,14 +362,31 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
         cols = [t[:n] for t in (out.f_final, out.grad_norm, out.iterations, out.status,
                                 out.ls_trials, out.grad_evals)]
         base = lo
-    host = [c.cpu().numpy() for c in cols]
-    x_host = np.ascontiguousarray(xs.cpu().numpy().T)
-    best_host = best_dev.cpu().numpy()
-    tallies_host = tallies.cpu().numpy()
-    pso_best = float(gbest[0].item()) if gbest is not None else math.nan
+    m_rows = xs.shape[1]
+    fpack = torch.empty((m_rows, d + 2), dtype=torch.float64, device=dev)
+    fpack[:, :d] = xs.t()
+    fpack[:, d] = cols[0]
+    fpack[:, d + 1] = cols[1]
+    ipack = torch.empty((m_rows, 4), dtype=torch.int32, device=dev)
+    for c, t in enumerate((cols[2], cols[3], cols[4], cols[5])):
+        ipack[:, c] = t
+    spack = torch.empty(5, dtype=torch.float64, device=dev)
+    spack[0:4] = tallies
+    spack[4] = gbest[0] if gbest is not None else math.nan
+    fh = torch.empty(fpack.shape, dtype=torch.float64, pin_memory=True)
+    ih = torch.empty(ipack.shape, dtype=torch.int32, pin_memory=True)
+    fh.copy_(fpack, non_blocking=True)
+    ih.copy_(ipack, non_blocking=True)
+    best_host = best_dev.cpu().numpy()  # (world > 1: every rank's [f, idx])
+    sh = spack.cpu().numpy()
     stream.synchronize()
     device_time = ev_start.elapsed_time(ev_end) / 1e3
-
+    fnp, inp = fh.numpy(), ih.numpy()
+    x_host = fnp[:, :d]
+    host = [fnp[:, d], fnp[:, d + 1], inp[:, 0], inp[:, 1].astype(np.uint8), inp[:, 2],
+            inp[:, 3]]
+    tallies_host = sh[0:4].astype(np.int64)
+    pso_best = float(sh[4])
     f_h, gn_h, it_h, st_h, ls_h, ge_h = host
     m = len(f_h)
     converged_count = int(tallies_host[0])

@@ -167,6 +167,19 @@ class SwarmShard:
         LAUNCHES[0] += 2
         self.sweeps_done += 1
 
+    def run_local(self, lower: float, upper: float, w: float, c1: float, c2: float,
+                  iter_pso: int) -> None:
+        """init + iter_pso sweeps + the barrier after each, when this shard is
+        the whole swarm (one GPU): one fused launch per sweep (zeus_pso_run)."""
+        _capi.check(_capi.lib().zeus_pso_run(
+            self.obj, self.d, self.n, self.i0, self.seed, float(lower), float(upper), float(w),
+            float(c1), float(c2), int(iter_pso), self.x.data_ptr(), self.v.data_ptr(),
+            self.p.data_ptr(), self.pval.data_ptr(), self.n, self.cand.data_ptr(),
+            self.gX.data_ptr(), self.gbest.data_ptr(), self.ws.data_ptr(), self._stream()),
+            "pso_run")
+        LAUNCHES[0] += 1 + int(iter_pso)
+        self.sweeps_done = int(iter_pso)
+
     def select(self, cands: torch.Tensor, ncand: int) -> None:
         """Global best across shard candidates (np.argmin order, pso.py:73-76)."""
         _capi.check(_capi.lib().zeus_minloc_select(

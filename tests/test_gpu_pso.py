@@ -148,3 +148,26 @@ def test_public_init_update_swarm(z):
     # same sequence through the engine in one go
     ref = _run_shards("rastrigin", 2, 30, 21, 6)
     assert np.array_equal(state.positions, ref["x"])
+
+
+@pytest.mark.parametrize("name,d,n,sweeps", [("rastrigin", 10, 65536, 20),
+                                             ("rosenbrock", 2, 1000, 10),
+                                             ("ackley", 50, 4097, 5),
+                                             ("goldstein_price", 2, 300, 3)])
+def test_fused_pso_run_matches_per_sweep_barriers(name, d, n, sweeps):
+    """zeus_pso_run (one launch per sweep, the last block reduces the
+    barrier) == init/sweep kernels + finalize + minloc_select, bit for bit."""
+    from paper_2603_28770_b200 import engine
+
+    dev = torch.device("cuda", 0)
+    lo, hi = BOXES[name]
+    a = engine.SwarmShard(OBJ[name], d, n, 0, 7, dev)
+    a.run_local(lo, hi, 0.5, 1.2, 1.5, sweeps)
+    b = engine.SwarmShard(OBJ[name], d, n, 0, 7, dev)
+    b.init(lo, hi)
+    engine.local_barrier(b)
+    for _ in range(sweeps):
+        b.sweep(0.5, 1.2, 1.5)
+        engine.local_barrier(b)
+    for t in ("x", "v", "p", "pval", "gX", "gbest", "cand"):
+        assert torch.equal(getattr(a, t), getattr(b, t)), t

@@ -74,6 +74,10 @@ struct BfgsWarp {
   const double* alpha_tab;
   HelperTask* task;
   double* xbuf[2];  // the two x buffers (helper mode needs to name them)
+  TermIdx tix;      // helper mode: this thread's term-pass indices (fixed per kernel)
+#ifdef ZEUS_PHASE_TIMING
+  long long _pt;  // phase clock (scripts/latency_probe.py)
+#endif
 
   // Evaluate a batch: NH == 0 -> eval_batch over the warp; NH > 0 -> publish
   // the task, all 32 (1+NH) threads run the term pass, warp 0 folds.
@@ -87,17 +91,22 @@ struct BfgsWarp {
         task->xsel = (x == xbuf[0]) ? 0 : 1;
       }
       __syncwarp();
+      PHASE(6);  // batch setup (alpha table, task)
       bar1(NT);  // A: task, x, p, alphas visible to the helpers
+      PHASE(7);  // barrier A
       const int nt = Obj::nterms(d);
       const int total = (B > 0 ? B : 1) * nt;
       bool oor = false;
       if (total > 0)
         term_pass<Obj, FastMath, NT>(B, nt, total, alphas, d, x, p, T, TT, A.tstride, A.bmax,
-                                     lane, oor);
-      if (bar1_or(NT, oor)) {  // B: every term written
+                                     lane, oor, &tix);
+      PHASE(8);  // warp 0's share of the term pass
+      const bool any_oor = bar1_or(NT, oor);
+      PHASE(9);  // barrier B (waits for the helpers' terms)
+      if (any_oor) {  // B: every term written
         if (total > 0)
           term_pass<Obj, PreciseMath, NT>(B, nt, total, alphas, d, x, p, T, TT, A.tstride,
-                                          A.bmax, lane, oor);
+                                          A.bmax, lane, oor, &tix);
         bar1(NT);
       }
       const int nb = B > 0 ? B : 1;
@@ -112,6 +121,7 @@ struct BfgsWarp {
         f = Obj::finish(acc, d, err);
       }
       __syncwarp();
+      PHASE(10);  // reference-order folds
       return f;
     }
   }
@@ -170,7 +180,9 @@ struct BfgsWarp {
   // Fresh start s from x0, or (rec != nullptr, helper mode) resume a start
   // promoted by the warp kernel from its carry record (bfgs_common.cuh).
   __device__ void run(const BfgsArgs& A, long long s, int lane, const double* rec = nullptr) {
-    PHASE_T0();
+#ifdef ZEUS_PHASE_TIMING
+    _pt = clock64();
+#endif
     const int d = A.d;
     const int C = (d + 31) >> 5;  // columns per lane
     double hreg[DR > 0 ? DR : 1];
@@ -180,6 +192,11 @@ struct BfgsWarp {
     for (int c = 0; c < (DR > 0 ? 1 : kMaxC); ++c) a_col[c] = b_col[c] = 0.0;
     double acc[Obj::NACC];
     double* TT = T + Obj::NACC * A.bmax * A.tstride;  // term tangents [KT][bmax][tstride]
+    double* atab = TT + Obj::KT * A.bmax * A.tstride;  // per-warp alpha window (32)
+    const int bdef = max(1, 32 / max(Obj::nterms(d), 1));  // trials filling one warp
+    atab[lane] = alpha_at(A, lane);
+    int atab_t0 = 0;
+    __syncwarp();
     double f0 = 0.0;
     int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
     double gnorm = __longlong_as_double(0x7ff0000000000000LL);
@@ -277,12 +294,14 @@ struct BfgsWarp {
       int src_row = 0;  // batch row of the accepted trial (its tangents in TT)
       {
         int t0 = 0;
-        int B = min(max(prev_trials, max(1, 32 / max(Obj::nterms(d), 1))), A.bmax);
+        int B = min(max(prev_trials, bdef), A.bmax);
         for (;;) {
           B = min(B, A.iter_ls + 1 - t0);
-          double* atab = TT + Obj::KT * A.bmax * A.tstride;  // per-warp alpha scratch
-          if (lane < B) atab[lane] = alpha_at(A, t0 + lane);
-          __syncwarp();
+          if (t0 != atab_t0) {  // the window's step lengths (t0 = 0: kept from the last round)
+            atab[lane] = alpha_at(A, t0 + lane);
+            atab_t0 = t0;
+            __syncwarp();
+          }
           double accb[Obj::NACC];
           const double fb = evalb(A, B, atab, d, TT, lane, accb);
           bool pass = false;
@@ -542,6 +561,8 @@ __global__ void __launch_bounds__(NH > 0 ? 32 * (NH + 1) : kBfgsWarps * 32,
   W.T = v;
   W.xbuf[0] = W.x;
   W.xbuf[1] = W.xn;
+  if constexpr (NH > 0) W.tix = term_idx<32 * (NH + 1)>(Obj::nterms(d) > 0 ? Obj::nterms(d) : 1,
+                                                      (int)threadIdx.x);
   W.task = reinterpret_cast<HelperTask*>(sm + A.nalpha + A.warp_doubles);
 
   if constexpr (NH == 0) {
@@ -591,11 +612,11 @@ __global__ void __launch_bounds__(NH > 0 ? 32 * (NH + 1) : kBfgsWarps * 32,
       bool oor = false;
       if (total > 0)
         term_pass<Obj, FastMath, 32 * (NH + 1)>(B, nt, total, atab, d, x, W.p, W.T, TT,
-                                               A.tstride, A.bmax, tid, oor);
+                                               A.tstride, A.bmax, tid, oor, &W.tix);
       if (bar1_or(32 * (NH + 1), oor)) {  // B
         if (total > 0)
           term_pass<Obj, PreciseMath, 32 * (NH + 1)>(B, nt, total, atab, d, x, W.p, W.T, TT,
-                                                    A.tstride, A.bmax, tid, oor);
+                                                    A.tstride, A.bmax, tid, oor, &W.tix);
         bar1(32 * (NH + 1));
       }
     }
@@ -745,10 +766,10 @@ int zeus_debug_team_phase_cycles(unsigned long long* out, int reset) {
   return zeus::team_phase_cycles(out, reset);
 }
 int zeus_debug_phase_cycles(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, zeus_phase_cycles, sizeof(unsigned long long) * 8) != cudaSuccess)
+  if (cudaMemcpyFromSymbol(out, zeus_phase_cycles, sizeof(unsigned long long) * 16) != cudaSuccess)
     return -2;
   if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[16] = {};
     cudaMemcpyToSymbol(zeus_phase_cycles, z, sizeof(z));
   }
   return 0;

@@ -66,7 +66,7 @@ constexpr int kU = ZEUS_TERM_UNROLL;  // independent objective terms per lane pe
 // of every warp adds clock64() deltas into zeus_phase_cycles[] (diagnostics
 // for the latency probe, scripts/latency_probe.py; off in normal builds).
 #ifdef ZEUS_PHASE_TIMING
-__device__ unsigned long long zeus_phase_cycles[8];
+__device__ unsigned long long zeus_phase_cycles[16];
 #define PHASE_T0() long long _pt = clock64()
 #define PHASE(i)                                                  \
   do {                                                            \
@@ -129,13 +129,26 @@ __device__ __forceinline__ void warp_sum8(double v[8]) {
 // Term pass of a batch: (trial b, term j) pairs q = b * nt + j are spread over
 // the lanes, four independent terms per lane per step (their libm chains
 // overlap); (b, j) advance incrementally, no integer division per term.
+// Thread -> first (trial, term) item and the per-step increments of a term
+// pass; fixed for a kernel (d fixed), so helper CTAs compute it once.
+struct TermIdx {
+  int b0, j0, step_b, step_j;
+};
+template <int NTH>
+__device__ __forceinline__ TermIdx term_idx(int nt, int lane) {
+  const int step_b = NTH / nt;
+  const int b = lane / nt;
+  return TermIdx{b, lane - b * nt, step_b, NTH - step_b * nt};
+}
+
 template <class Obj, class M, int NTH = 32>
 __device__ __forceinline__ void term_pass(int B, int nt, int total, const double* alpha_of,
                                           int d, const double* x, const double* p, double* T,
                                           double* TT, int tstride, int rows, int lane,
-                                          bool& oor) {
-  const int step_b = NTH / nt, step_j = NTH - step_b * nt;
-  int b = lane / nt, j = lane - b * nt;
+                                          bool& oor, const TermIdx* pre = nullptr) {
+  const TermIdx ix = pre ? *pre : term_idx<NTH>(nt, lane);
+  const int step_b = ix.step_b, step_j = ix.step_j;
+  int b = ix.b0, j = ix.j0;
   for (int q0 = lane; q0 < total; q0 += NTH * kU) {
     double t[kU][Obj::NACC], tn[kU][Obj::KT];
     int bb[kU], jj[kU];

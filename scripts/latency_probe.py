@@ -29,7 +29,7 @@ import ctypes
 from paper_2603_28770_b200 import _capi
 L = _capi.lib()
 timing = hasattr(L, "zeus_debug_phase_cycles")
-buf = (ctypes.c_ulonglong * 8)()
+buf = (ctypes.c_ulonglong * 16)()
 for rep in range(3):
     if timing:
         torch.cuda.synchronize(); L.zeus_debug_phase_cycles(buf, 1); L.zeus_debug_team_phase_cycles(buf, 1)
@@ -39,7 +39,8 @@ for rep in range(3):
 k = int(out.iterations[0].item())
 if timing:
     L.zeus_debug_phase_cycles(buf, 0)
-    names = ["line search", "gradient", "H pass", "8-value reduction+p'", "ddir+swap", "prologue"]
+    names = ["line search (rest)", "gradient", "H pass", "8-value reduction+p'", "ddir+swap",
+             "prologue", "LS setup", "bar A", "term pass (warp 0)", "bar B", "folds"]
     print("warp phase cycles per iteration:", {n: round(buf[i] / max(k, 1)) for i, n in enumerate(names)})
     L.zeus_debug_team_phase_cycles(buf, 0)
     tn = ["line search", "gradient", "H pass", "8-value reduction+p'", "ddir"]

@@ -26,7 +26,7 @@ cfg = z.ZeusConfig(N=N, dim=d, range=(spec.lower, spec.upper), iter_pso=sweeps, 
                    seed=42, deterministic=True)
 L = _capi.lib()
 timing = hasattr(L, "zeus_debug_team_phase_cycles")
-buf = (ctypes.c_ulonglong * 8)()
+buf = (ctypes.c_ulonglong * 16)()
 z.zeus_run(spec.fn, cfg)  # warm-up
 torch.cuda.synchronize()
 if timing:

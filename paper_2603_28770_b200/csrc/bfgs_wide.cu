@@ -45,6 +45,10 @@ namespace zeus {
 namespace {
 
 constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
+#ifndef ZEUS_WIDE_SMEM_STEP
+#define ZEUS_WIDE_SMEM_STEP 4  // <= 4 (four accumulators per column)
+#endif
+static_assert(ZEUS_WIDE_SMEM_STEP >= 1 && ZEUS_WIDE_SMEM_STEP <= 4, "smem rows per step");
 #ifndef ZEUS_WIDE_UFROMP
 #define ZEUS_WIDE_UFROMP 1
 #endif
@@ -446,10 +450,13 @@ struct WideStart {
       if (own1) reinterpret_cast<double2*>(rowv + 4 * c1)[0] = make_double2(dg1, gn1);
       team_sync();
 
-      // ---- fused pass over my two columns: lazy update, w = H g' (u = w + p)
+      // ---- fused pass over my two columns: lazy update, w = H g' (u = w + p).
+      // Four accumulators per column (rows i mod 4) so a warp keeps 8
+      // independent DFMA chains in flight (FP64 latency ~23 cycles).
       double u0 = 0.0, w0 = 0.0, u1 = 0.0, w1 = 0.0;
       {
-        double u0b = 0.0, w0b = 0.0, u1b = 0.0, w1b = 0.0;
+        double wa[4] = {0.0, 0.0, 0.0, 0.0}, wb[4] = {0.0, 0.0, 0.0, 0.0};
+        double ua[4] = {0.0, 0.0, 0.0, 0.0}, ub[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int i = 0; i < RR; ++i) {
           const double2 ra = *reinterpret_cast<const double2*>(rowv + 4 * i);      // dg, g'
@@ -458,48 +465,44 @@ struct WideStart {
           const double e1 = pending ? fma(rb.x, a1, fma(rb.y, b1, h1[i])) : h1[i];
           h0[i] = e0;
           h1[i] = e1;
-          if (i & 1) {
-            UACC(u0b = fma(e0, ra.x, u0b));
-            w0b = fma(e0, ra.y, w0b);
-            UACC(u1b = fma(e1, ra.x, u1b));
-            w1b = fma(e1, ra.y, w1b);
-          } else {
-            UACC(u0 = fma(e0, ra.x, u0));
-            w0 = fma(e0, ra.y, w0);
-            UACC(u1 = fma(e1, ra.x, u1));
-            w1 = fma(e1, ra.y, w1);
-          }
+          UACC(ua[i & 3] = fma(e0, ra.x, ua[i & 3]));
+          wa[i & 3] = fma(e0, ra.y, wa[i & 3]);
+          UACC(ub[i & 3] = fma(e1, ra.x, ub[i & 3]));
+          wb[i & 3] = fma(e1, ra.y, wb[i & 3]);
         }
-        // rows RR.. from shared memory, two per step with every load issued
+        // rows RR.. from shared memory, four per step with every load issued
         // before the arithmetic (the loads' latency overlaps)
         int i = RR;
-        for (; i + 1 < d; i += 2) {
-          const double2 ra = *reinterpret_cast<const double2*>(rowv + 4 * i);
-          const double2 rb = *reinterpret_cast<const double2*>(rowv + 4 * i + 2);
-          const double2 rc = *reinterpret_cast<const double2*>(rowv + 4 * i + 4);
-          const double2 rd = *reinterpret_cast<const double2*>(rowv + 4 * i + 6);
+        constexpr int SR = ZEUS_WIDE_SMEM_STEP;  // shared-memory rows per step
+        for (; i + SR - 1 < d; i += SR) {
+          double2 ra[SR], rb[SR];
+          double e0[SR], e1[SR];
           double* hr = Hs + (i - RR) * LD;
-          double e0 = hr[c0], e1 = hr[c1], f0v = hr[LD + c0], f1v = hr[LD + c1];
-          if (pending) {
-            e0 = fma(rb.x, a0, fma(rb.y, b0, e0));
-            e1 = fma(rb.x, a1, fma(rb.y, b1, e1));
-            f0v = fma(rd.x, a0, fma(rd.y, b0, f0v));
-            f1v = fma(rd.x, a1, fma(rd.y, b1, f1v));
-            hr[c0] = e0;
-            hr[c1] = e1;
-            hr[LD + c0] = f0v;
-            hr[LD + c1] = f1v;
+#pragma unroll
+          for (int r = 0; r < SR; ++r) {
+            ra[r] = *reinterpret_cast<const double2*>(rowv + 4 * (i + r));
+            rb[r] = *reinterpret_cast<const double2*>(rowv + 4 * (i + r) + 2);
+            e0[r] = hr[r * LD + c0];
+            e1[r] = hr[r * LD + c1];
           }
-          UACC(u0 = fma(e0, ra.x, u0));
-          w0 = fma(e0, ra.y, w0);
-          UACC(u1 = fma(e1, ra.x, u1));
-          w1 = fma(e1, ra.y, w1);
-          UACC(u0b = fma(f0v, rc.x, u0b));
-          w0b = fma(f0v, rc.y, w0b);
-          UACC(u1b = fma(f1v, rc.x, u1b));
-          w1b = fma(f1v, rc.y, w1b);
+          if (pending) {
+#pragma unroll
+            for (int r = 0; r < SR; ++r) {
+              e0[r] = fma(rb[r].x, a0, fma(rb[r].y, b0, e0[r]));
+              e1[r] = fma(rb[r].x, a1, fma(rb[r].y, b1, e1[r]));
+              hr[r * LD + c0] = e0[r];
+              hr[r * LD + c1] = e1[r];
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < SR; ++r) {
+            UACC(ua[r] = fma(e0[r], ra[r].x, ua[r]));
+            wa[r] = fma(e0[r], ra[r].y, wa[r]);
+            UACC(ub[r] = fma(e1[r], ra[r].x, ub[r]));
+            wb[r] = fma(e1[r], ra[r].y, wb[r]);
+          }
         }
-        if (i < d) {
+        for (; i < d; ++i) {
           const double2 ra = *reinterpret_cast<const double2*>(rowv + 4 * i);
           const double2 rb = *reinterpret_cast<const double2*>(rowv + 4 * i + 2);
           double* hr = Hs + (i - RR) * LD;
@@ -510,23 +513,23 @@ struct WideStart {
             hr[c0] = e0;
             hr[c1] = e1;
           }
-          UACC(u0b = fma(e0, ra.x, u0b));
-          w0b = fma(e0, ra.y, w0b);
-          UACC(u1b = fma(e1, ra.x, u1b));
-          w1b = fma(e1, ra.y, w1b);
+          UACC(ua[0] = fma(e0, ra.x, ua[0]));  // (the < SR remainder rows)
+          wa[0] = fma(e0, ra.y, wa[0]);
+          UACC(ub[0] = fma(e1, ra.x, ub[0]));
+          wb[0] = fma(e1, ra.y, wb[0]);
         }
-        w0 += w0b;
-        w1 += w1b;
+        w0 = (wa[0] + wa[1]) + (wa[2] + wa[3]);
+        w1 = (wb[0] + wb[1]) + (wb[2] + wb[3]);
 #if ZEUS_WIDE_UFROMP
         // u = H_k dg = H_k g' - H_k g = w + p: p = -H_k g is this iteration's
         // direction (exact in exact arithmetic), so the pass needs one matvec
         u0 = w0 + p0;
         u1 = w1 + p1;
-        (void)u0b;
-        (void)u1b;
+        (void)ua;
+        (void)ub;
 #else
-        u0 += u0b;
-        u1 += u1b;
+        u0 = (ua[0] + ua[1]) + (ua[2] + ua[3]);
+        u1 = (ub[0] + ub[1]) + (ub[2] + ub[3]);
 #endif
         if (!own0) u0 = w0 = 0.0;
         if (!own1) u1 = w1 = 0.0;

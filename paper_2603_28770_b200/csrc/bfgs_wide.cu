@@ -45,10 +45,7 @@ namespace zeus {
 namespace {
 
 constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
-#ifndef ZEUS_WIDE_SMEM_STEP
-#define ZEUS_WIDE_SMEM_STEP 4  // <= 4 (four accumulators per column)
-#endif
-static_assert(ZEUS_WIDE_SMEM_STEP >= 1 && ZEUS_WIDE_SMEM_STEP <= 4, "smem rows per step");
+
 #ifndef ZEUS_WIDE_UFROMP
 #define ZEUS_WIDE_UFROMP 1
 #endif
@@ -84,18 +81,32 @@ __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(k
 
 }  // namespace
 
-// Per-objective shape, tuned on B200 (scripts/wide_variants.sh +
-// scripts/phase_probe.py at d = 50): rows of H kept in registers (RR),
-// resident blocks per SM (MINB; 2 warps each) and trials per line-search
-// chunk (CH: Ackley needs 1.6 trials per iteration, Rosenbrock 2.7, Rastrigin
-// 6.2; SM-cycles per start-iteration for CH = 1 / 2 / 3 / 4: Rosenbrock 820 /
-// 770 / 781 / 793, Rastrigin 1781 / 1729 / 1746 / 1915, Ackley 1596 / 1854
-// (team kernel: 2884)).  W = 2 (64 < d <= 128) keeps 32 rows in registers.
+// Shape, tuned on B200 (scripts/wide_variants.sh + scripts/phase_probe.py at
+// d = 50): rows of H kept in registers (RR), resident blocks per SM (MINB; 2
+// warps each), trials per line-search chunk (CH: Ackley needs 1.6 trials per
+// iteration, Rosenbrock 2.7, Rastrigin 6.2; SM-cycles per start-iteration for
+// CH = 1 / 2 / 3 / 4: Rosenbrock 820 / 770 / 781 / 793, Rastrigin 1781 / 1729
+// / 1746 / 1915, Ackley 1596 / 1854 (team kernel: 2884)) and shared-memory H
+// rows per step of the fused pass (SR).
 template <class Obj, int W>
 struct WideShape {
-  static constexpr int RR = (W > 1 || Obj::kId == ZEUS_OBJ_ROSENBROCK) ? 32 : 16;
-  static constexpr int MINB = (W > 1 || Obj::kId == ZEUS_OBJ_ROSENBROCK) ? 4 : 5;
+  // W = 1: 20 register rows at 168 registers = 3 warps per SMSP (12 starts/SM;
+  // the per-SMSP register file caps 3 warps at 168); measured at d = 50
+  // (SM-cycles/start-iteration, RR/MINB/SR): Rosenbrock 772 (32/4/4) -> 713
+  // (20/6/2), Rastrigin 1688 -> 1556, Ackley 1331 -> 1320.  W = 2 (d <= 128):
+  // 32 rows, 4 blocks/SM, four shared-memory rows per step (2: 11% slower).
+  static constexpr int RR = W > 1 ? 32 : 20;
+#ifdef ZEUS_WIDE_MINB_OVERRIDE
+  static constexpr int MINB = ZEUS_WIDE_MINB_OVERRIDE;
+#else
+  static constexpr int MINB = W > 1 ? 4 : 6;
+#endif
   static constexpr int CH = Obj::kId == ZEUS_OBJ_ACKLEY ? 1 : 2;
+#ifdef ZEUS_WIDE_SMEM_STEP
+  static constexpr int SR = ZEUS_WIDE_SMEM_STEP;
+#else
+  static constexpr int SR = W > 1 ? 4 : 2;  // shared-memory rows per step (<= 4)
+#endif
 };
 
 // Shared-memory slice of one start, in doubles: rowv [64W][4], H rows
@@ -473,7 +484,8 @@ struct WideStart {
         // rows RR.. from shared memory, four per step with every load issued
         // before the arithmetic (the loads' latency overlaps)
         int i = RR;
-        constexpr int SR = ZEUS_WIDE_SMEM_STEP;  // shared-memory rows per step
+        constexpr int SR = WideShape<Obj, W>::SR;  // shared-memory rows per step
+        static_assert(SR >= 1 && SR <= 4, "four accumulators per column");
         for (; i + SR - 1 < d; i += SR) {
           double2 ra[SR], rb[SR];
           double e0[SR], e1[SR];

@@ -147,3 +147,30 @@ def test_full_size_config2_properties(z):
     assert np.array_equal(a.per_run.iterations, b.per_run.iterations)
     print(f"C2 full: {a.converged_count} converged, device {a.device_time*1e3:.2f} ms, "
           f"wall {a.wall_time*1e3:.1f} ms, best f {a.best.f_final:.3e}")
+
+
+@pytest.mark.parametrize("name,d,n,cap", [("rosenbrock", 50, 131072, 2000),
+                                          ("rastrigin", 50, 131072, 2000),
+                                          ("ackley", 50, 262144, 1000),
+                                          ("rosenbrock", 100, 131072, 2000)])
+def test_full_size_wide_configs_properties(z, name, d, n, cap):
+    """T50 (1M-start 50-D over 8 GPUs = 131,072 per GPU), config 3 and config 4
+    shards at full size through the wide kernels: converged <=> |g| < theta,
+    tallies, best <= PSO best, every k within the cap, per-start trial and
+    gradient counters consistent, and a second run bit-identical."""
+    spec = z.get_objective(name, d)
+    cfg = z.ZeusConfig(N=n, dim=d, range=(spec.lower, spec.upper), iter_pso=5, iter_bfgs=cap,
+                       seed=11, deterministic=True)
+    a = z.zeus_run(spec.fn, cfg)
+    pr = a.per_run
+    st = pr.status_codes
+    assert len(pr) == n
+    assert np.array_equal(st == 0, pr.grad_norm < cfg.theta)
+    assert a.converged_count == int(np.sum(st == 0)) and a.converged_count > 0.99 * n
+    assert a.best.f_final <= a.pso_best_before_bfgs
+    assert pr.iterations.min() >= 0 and pr.iterations.max() <= cap
+    it, ls, ge = a.stats.iterations, a.stats.ls_trials, a.stats.grad_evals
+    assert np.all(ls >= it) and np.all(ge <= it + 1)
+    b = z.zeus_run(spec.fn, cfg)
+    assert np.array_equal(a.per_run.x_final, b.per_run.x_final)
+    assert np.array_equal(a.per_run.iterations, b.per_run.iterations)

@@ -214,6 +214,14 @@ int zeus_user_set_data(void *handle, const double *data, void *stream);
  * objective raises DomainError */
 int zeus_user_value(void *handle, int64_t n, const double *x, int64_t ldx, double *f,
                     void *stream);
+/* forward_gradient (autodiff.py:243-266) / armijo_search (linesearch.py:40-71)
+ * on n points -- as zeus_objective_gradient / zeus_armijo; trials[i] = -1
+ * where the objective raised DomainError inside the search */
+int zeus_user_gradient(void *handle, int64_t n, const double *x, int64_t ldx, double *grad,
+                       uint8_t *domain_error, void *stream);
+int zeus_user_armijo(void *handle, int64_t n, const double *x, const double *p, const double *g,
+                     int64_t ld, const double *f0, const zeus_bfgs_params *params, double *alpha,
+                     int32_t *trials, void *stream);
 /* init_swarm / update_swarm (pso.py:79-164) -- as zeus_pso_init/_sweep */
 int zeus_user_pso_init(void *handle, int64_t n, int64_t i0, uint64_t seed, double lower,
                        double upper, double *x, double *v, double *pbest, double *pval,

@@ -75,6 +75,9 @@ _SIGNATURES = {
     "zeus_user_dim": (_int, [_vp]),
     "zeus_user_set_data": (_int, [_vp, _vp, _vp]),
     "zeus_user_value": (_int, [_vp, _i64, _vp, _i64, _vp, _vp]),
+    "zeus_user_gradient": (_int, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "zeus_user_armijo": (_int, [_vp, _i64, _vp, _vp, _vp, _i64, _vp, ctypes.POINTER(BfgsParams),
+                                _vp, _vp, _vp]),
     "zeus_user_pso_init": (_int, [_vp, _i64, _i64, _u64, _dbl, _dbl, _vp, _vp, _vp, _vp, _i64,
                                   _vp, _vp, _vp]),
     "zeus_user_pso_sweep": (_int, [_vp, _i64, _i64, _u64, _int, _dbl, _dbl, _dbl, _vp, _vp, _vp,

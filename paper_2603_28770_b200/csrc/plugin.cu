@@ -33,7 +33,7 @@ constexpr size_t kUserWsHeader = 256;
 struct UserPlugin {
   CUmodule mod = nullptr;
   CUfunction pso_init = nullptr, pso_sweep = nullptr, pso_finalize = nullptr, bfgs = nullptr,
-             value = nullptr;
+             value = nullptr, gradient = nullptr, armijo = nullptr;
   CUdeviceptr data_sym = 0;
   int d = 0;
 };
@@ -131,7 +131,9 @@ int zeus_user_compile(const char* source, int d, const char* include_dir, void**
   const std::string k_bfgs = "zeus::bfgs_thread_kernel<zeus::UserObj, " + std::to_string(d) + ">";
   const char* names[] = {"zeus::pso_init_kernel<zeus::UserObj>",
                          "zeus::pso_sweep_kernel<zeus::UserObj>", "zeus::pso_finalize_kernel",
-                         k_bfgs.c_str(), "zeus::user_value_kernel"};
+                         k_bfgs.c_str(), "zeus::user_value_kernel",
+                         "zeus::user_gradient_kernel", "zeus::user_armijo_kernel"};
+  constexpr int kNames = 7;
   for (const char* nm : names) nvrtcAddNameExpression(p, nm);
   const nvrtcResult cres = nvrtcCompileProgram(p, (int)(sizeof opts / sizeof opts[0]), opts);
   size_t log_n = 0;
@@ -147,16 +149,17 @@ int zeus_user_compile(const char* source, int d, const char* include_dir, void**
   rc = rtc_check(nvrtcGetCUBINSize(p, &cubin_n), "nvrtcGetCUBINSize");
   std::vector<char> cubin(cubin_n);
   if (!rc) rc = rtc_check(nvrtcGetCUBIN(p, cubin.data()), "nvrtcGetCUBIN");
-  const char* lowered[5] = {};
-  for (int i = 0; i < 5 && !rc; ++i)
+  const char* lowered[kNames] = {};
+  for (int i = 0; i < kNames && !rc; ++i)
     rc = rtc_check(nvrtcGetLoweredName(p, names[i], &lowered[i]), "nvrtcGetLoweredName");
   UserPlugin* up = nullptr;
   if (!rc) {
     up = new UserPlugin();
     up->d = d;
     rc = cu_check(drv().ModuleLoadData(&up->mod, cubin.data()), "cuModuleLoadData");
-    CUfunction* fs[5] = {&up->pso_init, &up->pso_sweep, &up->pso_finalize, &up->bfgs, &up->value};
-    for (int i = 0; i < 5 && !rc; ++i)
+    CUfunction* fs[kNames] = {&up->pso_init, &up->pso_sweep, &up->pso_finalize, &up->bfgs,
+                              &up->value, &up->gradient, &up->armijo};
+    for (int i = 0; i < kNames && !rc; ++i)
       rc = cu_check(drv().ModuleGetFunction(fs[i], up->mod, lowered[i]), "cuModuleGetFunction");
     size_t sym_n = 0;
     if (!rc)
@@ -213,6 +216,35 @@ int zeus_user_value(void* handle, int64_t n, const double* x, int64_t ldx, doubl
   return cu_check(drv().LaunchKernel(up->value, nb, 1, 1, 128, 1, 1, 0, (CUstream)stream, args,
                                  nullptr),
                   "user_value_kernel");
+}
+
+int zeus_user_gradient(void* handle, int64_t n, const double* x, int64_t ldx, double* grad,
+                       uint8_t* domain_error, void* stream) {
+  UserPlugin* up = (UserPlugin*)handle;
+  if (!up || n < 0 || ldx < n || (n > 0 && (!x || !grad || !domain_error)))
+    return set_error(ZEUS_ERR_ARGUMENT, "zeus_user_gradient: bad arguments");
+  if (n == 0) return ZEUS_OK;
+  int d = up->d;
+  void* args[] = {&d, &n, &x, &ldx, &grad, &domain_error};
+  return cu_check(drv().LaunchKernel(up->gradient, (unsigned)((n + 127) / 128), 1, 1, 128, 1, 1, 0,
+                                     (CUstream)stream, args, nullptr),
+                  "user_gradient_kernel");
+}
+
+int zeus_user_armijo(void* handle, int64_t n, const double* x, const double* p, const double* g,
+                     int64_t ld, const double* f0, const zeus_bfgs_params* P, double* alpha,
+                     int32_t* trials, void* stream) {
+  UserPlugin* up = (UserPlugin*)handle;
+  if (!up || n < 0 || ld < n || !P || (n > 0 && (!x || !p || !g || !f0 || !alpha || !trials)))
+    return set_error(ZEUS_ERR_ARGUMENT, "zeus_user_armijo: bad arguments");
+  if (n == 0) return ZEUS_OK;
+  int d = up->d;
+  double c1 = P->c1_armijo, a0 = P->alpha0, sh = P->shrink;
+  int il = P->iter_ls;
+  void* args[] = {&d, &n, &x, &p, &g, &ld, &f0, &c1, &a0, &il, &sh, &alpha, &trials};
+  return cu_check(drv().LaunchKernel(up->armijo, (unsigned)((n + 127) / 128), 1, 1, 128, 1, 1, 0,
+                                     (CUstream)stream, args, nullptr),
+                  "user_armijo_kernel");
 }
 
 static int finalize(UserPlugin* up, int nb, int64_t i0, double* p, int64_t ld, double* blk_f,

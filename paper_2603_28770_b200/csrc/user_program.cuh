@@ -65,4 +65,42 @@ __global__ void user_value_kernel(int d, int64_t n, const double* x, int64_t ldx
   f[i] = err ? __longlong_as_double(0x7ff8000000000000LL) : t[0];
 }
 
+// forward_gradient (autodiff.py:243-266) of n points: d seeded Dual passes
+__global__ void user_gradient_kernel(int d, int64_t n, const double* x, int64_t ldx, double* g,
+                                     uint8_t* domain_error) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xs[ZEUS_USER_D];
+  for (int k = 0; k < d; ++k) xs[k] = x[(int64_t)k * ldx + i];
+  bool err = false;
+  for (int k = 0; k < d; ++k)
+    g[(int64_t)k * ldx + i] = objective<Dual>(SeedX<PlainX>{PlainX{xs}, k}, d, zeus_user_data, err).d;
+  domain_error[i] = err ? 1 : 0;
+}
+
+// armijo_search (linesearch.py:40-71) on n problems; trials = -1 where the
+// objective raised DomainError (the reference propagates the exception)
+__global__ void user_armijo_kernel(int d, int64_t n, const double* x, const double* p,
+                                   const double* g, int64_t ld, const double* f0, double c1,
+                                   double alpha0, int iter_ls, double shrink, double* alpha_out,
+                                   int32_t* trials_out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ddir = 0.0;  // np.dot(g, p), sequential order
+  for (int k = 0; k < d; ++k) ddir = ddir + g[(int64_t)k * ld + i] * p[(int64_t)k * ld + i];
+  double alpha = alpha0, xt[ZEUS_USER_D];
+  int t = 0;
+  bool err = false;
+  for (;; ++t) {
+    for (int k = 0; k < d; ++k) xt[k] = x[(int64_t)k * ld + i] + alpha * p[(int64_t)k * ld + i];
+    const double ft = objective<double>(PlainX{xt}, d, zeus_user_data, err);
+    if (err) break;
+    if (ft <= f0[i] + c1 * alpha * ddir) break;  // NaN fails
+    if (t >= iter_ls) break;
+    alpha *= shrink;
+  }
+  alpha_out[i] = alpha;
+  trials_out[i] = err ? -1 : t + 1;
+}
+
 }  // namespace zeus

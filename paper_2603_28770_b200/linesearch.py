@@ -63,9 +63,6 @@ def armijo_search(
     g = np.asarray(g, dtype=np.float64)
     d = x.shape[0]
     obj = objective_id(f, d)
-    if not isinstance(obj, int):
-        raise NotImplementedError(f"armijo_search of a user DeviceObjective: call it through "
-                                  "bfgs_run / zeus_run (its gradient runs inside the BFGS kernel)")
     ddir = float(np.dot(g, p))
     if ddir >= 0.0:
         log.debug("line search entered with non-descent direction (g.p=%g)", ddir)
@@ -77,8 +74,20 @@ def armijo_search(
     alpha = torch.empty(1, dtype=torch.float64, device=dev)
     trials = torch.empty(1, dtype=torch.int32, device=dev)
     P = _params(params)
+    sp = _device.stream_ptr(dev)
+    if not isinstance(obj, int):  # user objective (plugin.DeviceObjective)
+        from .autodiff import DomainError
+
+        obj.bind(sp)
+        _capi.check(_capi.lib().zeus_user_armijo(obj.handle, 1, xs.data_ptr(), ps.data_ptr(),
+                                                 gs.data_ptr(), 1, f0s.data_ptr(), P,
+                                                 alpha.data_ptr(), trials.data_ptr(), sp),
+                    "armijo_search (user objective)")
+        if int(trials.item()) < 0:  # the reference lets the DomainError propagate
+            raise DomainError(f"{obj.name}: evaluation left the domain in the line search")
+        return float(alpha.item())
     _capi.check(_capi.lib().zeus_armijo(obj, d, 1, xs.data_ptr(), ps.data_ptr(), gs.data_ptr(),
                                         1, f0s.data_ptr(), P, alpha.data_ptr(),
-                                        trials.data_ptr(), _device.stream_ptr(dev)),
+                                        trials.data_ptr(), sp),
                 "armijo_search")
     return float(alpha.item())

@@ -113,8 +113,25 @@ __device__ T objective(const X& x, int d, const double* data, bool& err) {
         z.DeviceObjective("this is not C++", dim=2)
     with pytest.raises(ValueError):
         z.DeviceObjective(src, dim=17)
-    with pytest.raises(NotImplementedError):
-        z.forward_gradient(f, [1.0, 2.0])
+    g = z.forward_gradient(f, [3.0, 4.0])        # d|x|/dx = x / |x|
+    assert np.allclose(g, [0.6, 0.8], rtol=0, atol=1e-15)
+    with pytest.raises(z.DomainError):
+        z.forward_gradient(f, [0.0, 0.0])          # sqrt'(0), like the reference
+
+
+@pytest.mark.gpu
+def test_plugin_gradient_and_line_search_match_registered(z):
+    f = z.DeviceObjective(RASTRIGIN_SRC, dim=4, name="rastrigin_plugin")
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        x = rng.uniform(-4, 4, 4)
+        g_user = z.forward_gradient(f, x)
+        g_reg = z.forward_gradient(z.rastrigin, x)
+        assert np.array_equal(g_user, g_reg)        # same Dual rules, same order
+        p = -g_reg
+        ls = z.LineSearchParams()
+        assert z.armijo_search(f, x, p, g_reg, z.rastrigin(list(x)), ls) == \
+            z.armijo_search(z.rastrigin, x, p, g_reg, z.rastrigin(list(x)), ls)
 
 
 @pytest.mark.gpu

@@ -40,14 +40,19 @@
 
 namespace zeus {
 
-// Named-barrier helpers for the helper-warp mode (warp 0 and the helpers
-// meet at barrier 1 from different code paths, which PTX bar.sync permits).
-__device__ __forceinline__ void bar1(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+// Named-barrier helpers for the helper-warp mode.  Warp 0 and the helpers
+// meet at barrier 1 from different code locations, so these are the
+// NON-aligned forms (barrier.sync / barrier.red): bar.sync is
+// barrier.sync.aligned, which requires every thread to execute the same
+// instruction (compute-sanitizer synccheck flags it).
+__device__ __forceinline__ void bar1(int n) {
+  asm volatile("barrier.sync 1, %0;" ::"r"(n) : "memory");
+}
 __device__ __forceinline__ bool bar1_or(int n, bool v) {
   int r;
   asm volatile(
       "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\t"
-      "bar.red.or.pred q, 1, %2, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
+      "barrier.red.or.pred q, 1, %2, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
       : "=r"(r)
       : "r"((int)v), "r"(n)
       : "memory");

@@ -723,6 +723,10 @@ static int launch_helpers(BfgsArgs A, const BfgsPlan& P, cudaStream_t s) {
   return check_launch("bfgs_warp_kernel(helpers)");
 }
 
+#ifndef ZEUS_NH
+#define ZEUS_NH 7  // helper warps per straggler CTA (tier 3)
+#endif
+
 struct BfgsResumeLaunch {
   template <class Obj>
   static int run(BfgsArgs A, cudaStream_t s) {
@@ -732,8 +736,8 @@ struct BfgsResumeLaunch {
     A.tstride = P.tstride;
     A.bmax = P.bmax;
     A.nalpha = P.nalpha;
-    if (P.dr == 16) return launch_helpers<Obj, 16, 7>(A, P, s);
-    if (P.dr == 32) return launch_helpers<Obj, 32, 7>(A, P, s);
+    if (P.dr == 16) return launch_helpers<Obj, 16, ZEUS_NH>(A, P, s);
+    if (P.dr == 32) return launch_helpers<Obj, 32, ZEUS_NH>(A, P, s);
     return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs resume: d=%d", A.d);
   }
 };

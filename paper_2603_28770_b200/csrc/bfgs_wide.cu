@@ -396,7 +396,12 @@ struct WideStart {
           double v[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) v[q] = q < CH * NA ? sc[q % CH][q / CH] : 0.0;
-          team_sum8(v, l);
+          if constexpr (W == 1 && CH * NA <= 2) {
+#pragma unroll
+            for (int q = 0; q < CH * NA; ++q) v[q] = warp_sum(v[q]);  // 2 butterflies
+          } else {
+            team_sum8(v, l);  // transpose-reduce
+          }
           unsigned pm = 0u;
           double fb[CH];
 #pragma unroll

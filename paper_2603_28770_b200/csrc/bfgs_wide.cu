@@ -162,6 +162,28 @@ struct WideStart {
       }
     }
   }
+  // v[0], v[1] summed over the team (butterflies: 10 shuffles instead of 17)
+  __device__ __forceinline__ void team_sum2(double v[8], int l) {
+    v[0] = warp_sum(v[0]);
+    v[1] = warp_sum(v[1]);
+    if constexpr (W > 1) {
+      double* r = xch + slot * 8 * W;
+      slot ^= 1;
+      if (l == 0) {
+        r[wi * 8] = v[0];
+        r[wi * 8 + 1] = v[1];
+      }
+      __syncthreads();
+      double s0 = r[0], s1 = r[1];
+#pragma unroll
+      for (int w = 1; w < W; ++w) {
+        s0 += r[w * 8];
+        s1 += r[w * 8 + 1];
+      }
+      v[0] = s0;
+      v[1] = s1;
+    }
+  }
   __device__ __forceinline__ double team_sum(double v, int l) {
     v = warp_sum(v);
     if constexpr (W > 1) {
@@ -396,9 +418,8 @@ struct WideStart {
           double v[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) v[q] = q < CH * NA ? sc[q % CH][q / CH] : 0.0;
-          if constexpr (W == 1 && CH * NA <= 2) {
-#pragma unroll
-            for (int q = 0; q < CH * NA; ++q) v[q] = warp_sum(v[q]);  // 2 butterflies
+          if constexpr (CH * NA <= 2) {
+            team_sum2(v, l);  // butterflies (+ the warp totals for W = 2)
           } else {
             team_sum8(v, l);  // transpose-reduce
           }

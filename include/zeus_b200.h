@@ -124,6 +124,31 @@ int zeus_pso_run(int obj, int d, int64_t n, int64_t i0, uint64_t seed, double lo
                  double upper, double w, double c1, double c2, int iter_pso, double *x,
                  double *v, double *pbest, double *pval, int64_t ld, double *cand, double *gX,
                  double *gbest, void *workspace, void *stream);
+/* Multi-GPU PSO phase with the global-best barrier done INSIDE each sweep
+ * kernel over peer memory (pso.py:73-76 + driver.py:236-241 across shards; the
+ * reference's per-sweep host reduction, replaced here by NVLink stores): each
+ * rank owns an exchange block of zeus_pso_xchg_bytes(d, world) bytes
+ * (zeus_ipc_alloc; peers map it with zeus_ipc_open), initialised once by
+ * zeus_pso_xchg_setup with every rank's block as mapped in this process
+ * (bases[world], bases[rank] == block).  zeus_pso_run_xchg then runs init +
+ * iter_pso sweeps of this rank's shard [i0, i0 + n) (n may be 0); the last
+ * block of each launch publishes the shard candidate to every rank, waits
+ * for all ranks' candidates of the same exchange and writes the np.argmin
+ * winner to gX[d] / gbest[2].  Exchanges are numbered seq0, seq0 + 1, ...,
+ * seq0 + iter_pso; every rank passes the same seq0 (>= 1), and the next call
+ * continues the numbering at seq0 + iter_pso + 1.  A peer that never arrives
+ * within 20 s sets the timeout word (zeus_pso_xchg_status) instead of
+ * hanging.  world <= 8.  Results identical to zeus_pso_init / zeus_pso_sweep
+ * + an all-gather + zeus_minloc_select over the same shards. */
+size_t zeus_pso_xchg_bytes(int d, int world);
+int zeus_pso_xchg_setup(void *block, int d, int rank, int world, void *const *bases,
+                        void *stream);
+int zeus_pso_xchg_status(const void *block, int d, int world, unsigned *timed_out);
+int zeus_pso_run_xchg(int obj, int d, int64_t n, int64_t i0, uint64_t seed, double lower,
+                      double upper, double w, double c1, double c2, int iter_pso, double *x,
+                      double *v, double *pbest, double *pval, int64_t ld, double *cand,
+                      double *gX, double *gbest, void *workspace, void *xchg_block, int world,
+                      unsigned long long seq0, void *stream);
 /* _reduce_global_best across shards (pso.py:73-76): cands[ncand][d+2] from
  * every shard (e.g. an NCCL all-gather); writes the np.argmin winner to
  * gX[d] and gbest[2] = {f, (double)global_index}. */
@@ -189,6 +214,12 @@ int zeus_count_within(int d, int64_t n, const double *x, int64_t ldx, const doub
  * zeus_bfgs's stop_counter / stop_flag.  The BFGS kernels use system-scope
  * atomics and volatile flag loads, so the counter is coherent across GPUs
  * over NVLink / NVSwitch.  Layout: u64 counter at offset 0, i32 flag at 8. */
+/* device memory of its own cudaMalloc (so an IPC handle maps exactly it),
+ * zeroed; handle: ZEUS_IPC_HANDLE_BYTES.  zeus_ipc_open maps a peer's block
+ * (peer access enabled lazily); zeus_ipc_close frees (owner) or unmaps. */
+int zeus_ipc_alloc(size_t bytes, void **block, unsigned char *handle);
+int zeus_ipc_open(const unsigned char *handle, void **block);
+int zeus_ipc_close(void *block, int owner);
 #define ZEUS_STOP_BLOCK_BYTES 64
 #define ZEUS_IPC_HANDLE_BYTES 64
 int zeus_stop_block_create(void **block, unsigned char *handle);
@@ -230,6 +261,14 @@ int zeus_user_pso_sweep(void *handle, int64_t n, int64_t i0, uint64_t seed, int 
                         double w, double c1, double c2, double *x, double *v, double *pbest,
                         double *pval, int64_t ld, const double *gX, double *cand,
                         void *workspace, void *stream);
+/* zeus_pso_run (xchg_block == NULL; n >= 1) / zeus_pso_run_xchg (exchange
+ * block of zeus_pso_xchg_bytes(d, world), set up as above) for a user
+ * objective. */
+int zeus_user_pso_run(void *handle, int64_t n, int64_t i0, uint64_t seed, double lower,
+                      double upper, double w, double c1, double c2, int iter_pso, double *x,
+                      double *v, double *pbest, double *pval, int64_t ld, double *cand,
+                      double *gX, double *gbest, void *workspace, void *xchg_block, int world,
+                      unsigned long long seq0, void *stream);
 /* bfgs_run over n starts (bfgs.py:80-156) -- as zeus_bfgs */
 size_t zeus_user_bfgs_workspace_bytes(void);
 int zeus_user_bfgs(void *handle, int64_t n, const double *x0, int64_t ldx,

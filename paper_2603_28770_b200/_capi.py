@@ -58,6 +58,12 @@ _SIGNATURES = {
     "zeus_minloc_select": (_int, [_int, _int, _vp, _vp, _vp, _vp]),
     "zeus_pso_run": (_int, [_int, _int, _i64, _i64, _u64, _dbl, _dbl, _dbl, _dbl, _dbl, _int,
                             _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "zeus_pso_xchg_bytes": (_sz, [_int, _int]),
+    "zeus_pso_xchg_setup": (_int, [_vp, _int, _int, _int, ctypes.POINTER(_vp), _vp]),
+    "zeus_pso_xchg_status": (_int, [_vp, _int, _int, ctypes.POINTER(ctypes.c_uint)]),
+    "zeus_pso_run_xchg": (_int, [_int, _int, _i64, _i64, _u64, _dbl, _dbl, _dbl, _dbl, _dbl,
+                                 _int, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _int,
+                                 ctypes.c_ulonglong, _vp]),
     "zeus_bfgs_workspace_bytes": (_sz, [_int, _i64]),
     "zeus_bfgs": (_int, [_int, _int, _i64, _vp, _i64, ctypes.POINTER(BfgsParams), _i64, _vp,
                          _vp, ctypes.POINTER(BfgsOut), _vp, _vp]),
@@ -82,9 +88,15 @@ _SIGNATURES = {
                                   _vp, _vp, _vp]),
     "zeus_user_pso_sweep": (_int, [_vp, _i64, _i64, _u64, _int, _dbl, _dbl, _dbl, _vp, _vp, _vp,
                                    _vp, _i64, _vp, _vp, _vp, _vp]),
+    "zeus_user_pso_run": (_int, [_vp, _i64, _i64, _u64, _dbl, _dbl, _dbl, _dbl, _dbl, _int,
+                                 _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _int,
+                                 ctypes.c_ulonglong, _vp]),
     "zeus_user_bfgs_workspace_bytes": (_sz, []),
     "zeus_user_bfgs": (_int, [_vp, _i64, _vp, _i64, ctypes.POINTER(BfgsParams), _i64, _vp, _vp,
                               ctypes.POINTER(BfgsOut), _vp, _vp]),
+    "zeus_ipc_alloc": (_int, [_sz, ctypes.POINTER(_vp), ctypes.c_char_p]),
+    "zeus_ipc_open": (_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "zeus_ipc_close": (_int, [_vp, _int]),
     "zeus_stop_block_create": (_int, [ctypes.POINTER(_vp), ctypes.c_char_p]),
     "zeus_stop_block_open": (_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "zeus_stop_block_close": (_int, [_vp, _int]),

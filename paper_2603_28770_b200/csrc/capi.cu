@@ -295,12 +295,12 @@ int zeus_count_within(int d, int64_t n, const double* x, int64_t ldx, const doub
 // 64 bytes of cudaMalloc'ed device memory: counter (u64) at 0, flag (i32) at 8.
 // Its own allocation, so the IPC handle maps exactly this block (torch's
 // caching allocator would hand out an offset into a larger segment).
-int zeus_stop_block_create(void** dptr, unsigned char* handle) {
-  if (!dptr || !handle) return set_error(ZEUS_ERR_ARGUMENT, "zeus_stop_block_create");
+int zeus_ipc_alloc(size_t bytes, void** dptr, unsigned char* handle) {
+  if (!dptr || !handle || bytes == 0) return set_error(ZEUS_ERR_ARGUMENT, "zeus_ipc_alloc");
   void* p = nullptr;
-  int rc = check_cuda(cudaMalloc(&p, ZEUS_STOP_BLOCK_BYTES), "cudaMalloc(stop block)");
+  int rc = check_cuda(cudaMalloc(&p, bytes), "cudaMalloc(ipc block)");
   if (rc) return rc;
-  rc = check_cuda(cudaMemset(p, 0, ZEUS_STOP_BLOCK_BYTES), "cudaMemset(stop block)");
+  rc = check_cuda(cudaMemset(p, 0, bytes), "cudaMemset(ipc block)");
   cudaIpcMemHandle_t h;
   if (!rc) rc = check_cuda(cudaIpcGetMemHandle(&h, p), "cudaIpcGetMemHandle");
   if (rc) {
@@ -312,19 +312,29 @@ int zeus_stop_block_create(void** dptr, unsigned char* handle) {
   return ZEUS_OK;
 }
 
-int zeus_stop_block_open(const unsigned char* handle, void** dptr) {
-  if (!dptr || !handle) return set_error(ZEUS_ERR_ARGUMENT, "zeus_stop_block_open");
+int zeus_ipc_open(const unsigned char* handle, void** dptr) {
+  if (!dptr || !handle) return set_error(ZEUS_ERR_ARGUMENT, "zeus_ipc_open");
   cudaIpcMemHandle_t h;
   memcpy(&h, handle, sizeof(h));
   return check_cuda(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess),
                     "cudaIpcOpenMemHandle");
 }
 
-int zeus_stop_block_close(void* dptr, int owner) {
+int zeus_ipc_close(void* dptr, int owner) {
   if (!dptr) return ZEUS_OK;
-  return owner ? check_cuda(cudaFree(dptr), "cudaFree(stop block)")
+  return owner ? check_cuda(cudaFree(dptr), "cudaFree(ipc block)")
                : check_cuda(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
 }
+
+int zeus_stop_block_create(void** dptr, unsigned char* handle) {
+  return zeus_ipc_alloc(ZEUS_STOP_BLOCK_BYTES, dptr, handle);
+}
+
+int zeus_stop_block_open(const unsigned char* handle, void** dptr) {
+  return zeus_ipc_open(handle, dptr);
+}
+
+int zeus_stop_block_close(void* dptr, int owner) { return zeus_ipc_close(dptr, owner); }
 
 int zeus_stop_block_reset(void* dptr, void* stream) {
   if (!dptr) return set_error(ZEUS_ERR_ARGUMENT, "zeus_stop_block_reset");

@@ -269,8 +269,9 @@ int zeus_user_pso_init(void* handle, int64_t n, int64_t i0, uint64_t seed, doubl
   double range = upper - lower, vr = upper - lower;  // pso.py:101
   double vlow = -vr, vrange = vr - (-vr);
   void* none = nullptr;
+  unsigned long long seq = 0;  // no peer exchange on this path
   void* args[] = {&d, &n, &i0, &seed, &lower, &range, &vlow, &vrange, &x, &v, &pbest, &pval,
-                  &ld, &blk_f, &blk_i, &none, &none, &none, &none};
+                  &ld, &blk_f, &blk_i, &none, &none, &none, &none, &none, &seq};
   int rc = cu_check(drv().LaunchKernel(up->pso_init, nb, 1, 1, kPsoBlockU, 1, 1, 0, (CUstream)stream,
                                    args, nullptr),
                     "pso_init_kernel(user)");
@@ -292,13 +293,58 @@ int zeus_user_pso_sweep(void* handle, int64_t n, int64_t i0, uint64_t seed, int 
   long long* blk_i = (long long*)(blk_f + nb);
   uint64_t k0 = (uint64_t)(2 * d) * (uint64_t)(sweep + 1);
   void* none = nullptr;
+  unsigned long long seq = 0;  // no peer exchange on this path
   void* args[] = {&d, &n, &i0, &seed, &k0, &w, &c1, &c2, &x, &v, &pbest, &pval, &ld, &gX,
-                  &blk_f, &blk_i, &none, &none, &none, &none};
+                  &blk_f, &blk_i, &none, &none, &none, &none, &none, &seq};
   int rc = cu_check(drv().LaunchKernel(up->pso_sweep, nb, 1, 1, kPsoBlockU, 1, 1, 0,
                                    (CUstream)stream, args, nullptr),
                     "pso_sweep_kernel(user)");
   if (rc) return rc;
   return finalize(up, nb, i0, pbest, ld, blk_f, blk_i, cand, (CUstream)stream);
+}
+
+// The fused PSO phase of a user objective (zeus_pso_run / zeus_pso_run_xchg
+// with the NVRTC-compiled kernels): init + iter_pso sweeps, one launch each,
+// the last block writes the barrier's result; xchg_block != NULL adds the
+// multi-GPU peer-memory exchange (exchanges seq0 ...).
+int zeus_user_pso_run(void* handle, int64_t n, int64_t i0, uint64_t seed, double lower,
+                      double upper, double w, double c1, double c2, int iter_pso, double* x,
+                      double* v, double* pbest, double* pval, int64_t ld, double* cand,
+                      double* gX, double* gbest, void* workspace, void* xchg_block, int world,
+                      unsigned long long seq0, void* stream) {
+  UserPlugin* up = (UserPlugin*)handle;
+  if (!up || n < 0 || (n == 0 && !xchg_block) || i0 < 0 || ld < n || ld < 1 ||
+      !(lower < upper) || iter_pso < 0 || !x || !v || !pbest || !pval || !cand || !gX ||
+      !gbest || !workspace || (xchg_block && (world < 1 || world > 8 || seq0 < 1)))
+    return set_error(ZEUS_ERR_ARGUMENT, "zeus_user_pso_run: bad arguments");
+  int d = up->d;
+  CUstream s = (CUstream)stream;
+  int nb = n > 0 ? (int)((n + kPsoBlockU - 1) / kPsoBlockU) : 1;
+  double* blk_f = (double*)workspace;
+  long long* blk_i = (long long*)(blk_f + nb);
+  unsigned* done = (unsigned*)(blk_i + nb);
+  void* xg = xchg_block ? (char*)xchg_block + xchg_desc_offset(d, world) : nullptr;
+  int rc = check_cuda(cudaMemsetAsync(done, 0, sizeof(unsigned), (cudaStream_t)stream),
+                      "memset(pso done)");
+  if (rc) return rc;
+  double range = upper - lower, vr = upper - lower;  // pso.py:101
+  double vlow = -vr, vrange = vr - (-vr);
+  unsigned long long seq = seq0;
+  void* a_init[] = {&d, &n, &i0, &seed, &lower, &range, &vlow, &vrange, &x, &v, &pbest, &pval,
+                    &ld, &blk_f, &blk_i, &done, &cand, &gX, &gbest, &xg, &seq};
+  rc = cu_check(drv().LaunchKernel(up->pso_init, nb, 1, 1, kPsoBlockU, 1, 1, 0, s, a_init,
+                                   nullptr),
+                "pso_init_kernel(user, fused)");
+  for (int sw = 0; sw < iter_pso && !rc; ++sw) {
+    uint64_t k0 = (uint64_t)(2 * d) * (uint64_t)(sw + 1);
+    unsigned long long sq = seq0 + 1 + (unsigned)sw;
+    void* a_sw[] = {&d, &n, &i0, &seed, &k0, &w, &c1, &c2, &x, &v, &pbest, &pval, &ld, &gX,
+                    &blk_f, &blk_i, &done, &cand, &gX, &gbest, &xg, &sq};
+    rc = cu_check(drv().LaunchKernel(up->pso_sweep, nb, 1, 1, kPsoBlockU, 1, 1, 0, s, a_sw,
+                                     nullptr),
+                  "pso_sweep_kernel(user, fused)");
+  }
+  return rc;
 }
 
 size_t zeus_user_bfgs_workspace_bytes(void) { return kUserWsHeader; }

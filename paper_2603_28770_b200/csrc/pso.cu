@@ -18,7 +18,7 @@ struct PsoInitLaunch {
     const double vlow = -vr, vrange = vr - (-vr);
     pso_init_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, lower, range, vlow, vrange,
                                                   x, v, p, pval, ld, blk_f, blk_i, nullptr,
-                                                  nullptr, nullptr, nullptr);
+                                                  nullptr, nullptr, nullptr, nullptr, 0ull);
     int rc = check_launch("pso_init_kernel");
     if (rc) return rc;
     pso_finalize_kernel<<<1, kPsoBlock, 0, s>>>(d, nb, i0, p, ld, blk_f, blk_i, cand);
@@ -37,7 +37,7 @@ struct PsoSweepLaunch {
     const uint64_t k0 = (uint64_t)(2 * d) * (uint64_t)(sweep + 1);
     pso_sweep_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, k0, w, c1, c2, x, v, p,
                                                    pval, ld, gX, blk_f, blk_i, nullptr, nullptr,
-                                                   nullptr, nullptr);
+                                                   nullptr, nullptr, nullptr, 0ull);
     int rc = check_launch("pso_sweep_kernel");
     if (rc) return rc;
     pso_finalize_kernel<<<1, kPsoBlock, 0, s>>>(d, nb, i0, p, ld, blk_f, blk_i, cand);
@@ -45,16 +45,20 @@ struct PsoSweepLaunch {
   }
 };
 
-// The whole PSO phase of one shard that is the whole swarm (one GPU): init +
-// iter_pso sweeps, each ONE launch whose last block reduces the candidate and
-// writes the global best (pso.py:73-76 over one shard), no host round trips.
+// The whole PSO phase of a shard: init + iter_pso sweeps, each ONE launch
+// whose last block reduces the candidate and writes the global best -- over
+// this shard alone when it is the whole swarm (one GPU, pso.py:73-76 over one
+// shard), or over every rank's shard through the peer-memory exchange `xg`
+// (exchange seq0, seq0+1, ...) -- no host round trips, no NCCL launches.
+// n == 0 (an empty shard of a multi-GPU run) launches one idle block that
+// still takes part in the exchange.
 struct PsoRunLaunch {
   template <class Obj>
   static int run(int d, int64_t n, int64_t i0, uint64_t seed, double lower, double upper,
                  double w, double c1, double c2, int iter_pso, double* x, double* v, double* p,
                  double* pval, int64_t ld, double* cand, double* gX, double* gbest, void* ws,
-                 cudaStream_t s) {
-    const int nb = (int)((n + kPsoBlock - 1) / kPsoBlock);
+                 const PsoXchg* xg, unsigned long long seq0, cudaStream_t s) {
+    const int nb = n > 0 ? (int)((n + kPsoBlock - 1) / kPsoBlock) : 1;
     double* blk_f = (double*)ws;
     long long* blk_i = (long long*)(blk_f + nb);
     unsigned* done = (unsigned*)(blk_i + nb);
@@ -63,18 +67,27 @@ struct PsoRunLaunch {
     const double range = upper - lower, vr = upper - lower;  // pso.py:101
     pso_init_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, lower, range, -vr,
                                                   vr - (-vr), x, v, p, pval, ld, blk_f, blk_i,
-                                                  done, cand, gX, gbest);
+                                                  done, cand, gX, gbest, xg, seq0);
     rc = check_launch("pso_init_kernel(fused)");
     for (int sw = 0; sw < iter_pso && !rc; ++sw) {
       const uint64_t k0 = (uint64_t)(2 * d) * (uint64_t)(sw + 1);
       pso_sweep_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, k0, w, c1, c2, x, v, p,
                                                      pval, ld, gX, blk_f, blk_i, done, cand, gX,
-                                                     gbest);
+                                                     gbest, xg, seq0 + 1 + (unsigned)sw);
       rc = check_launch("pso_sweep_kernel(fused)");
     }
     return rc;
   }
 };
+
+// Exchange block of one rank: [2][world][d+2] f64 slots, [2][world] u64
+// flags, a u32 timeout word (padded to 8 B), then the PsoXchg descriptor.
+static size_t xchg_slots_bytes(int d, int world) {
+  return (size_t)2 * world * (d + 2) * sizeof(double);
+}
+size_t xchg_desc_offset(int d, int world) {
+  return xchg_slots_bytes(d, world) + (size_t)2 * world * 8 + 8;
+}
 
 }  // namespace zeus
 
@@ -96,9 +109,71 @@ int zeus_pso_run(int obj, int d, int64_t n, int64_t i0, uint64_t seed, double lo
       !pbest || !pval || !cand || !gX || !gbest || !workspace ||
       (obj == ZEUS_OBJ_GOLDSTEIN_PRICE && d != 2))
     return set_error(ZEUS_ERR_ARGUMENT, "zeus_pso_run: bad arguments");
+  const PsoXchg* none = nullptr;
   const int rc = dispatch_objective<PsoRunLaunch>(obj, d, n, i0, seed, lower, upper, w, c1, c2,
                                                   iter_pso, x, v, pbest, pval, ld, cand, gX,
-                                                  gbest, workspace, as_stream(stream));
+                                                  gbest, workspace, none, 0ull,
+                                                  as_stream(stream));
+  if (rc == ZEUS_ERR_ARGUMENT) return set_error(rc, "unknown objective id %d", obj);
+  return rc;
+}
+
+size_t zeus_pso_xchg_bytes(int d, int world) {
+  if (d < 1 || world < 1 || world > kXchgMaxRanks) return 0;
+  return xchg_desc_offset(d, world) + sizeof(PsoXchg);
+}
+
+int zeus_pso_xchg_setup(void* block, int d, int rank, int world, void* const* bases,
+                        void* stream) {
+  if (!block || !bases || d < 1 || world < 1 || world > kXchgMaxRanks || rank < 0 ||
+      rank >= world || bases[rank] != block)
+    return set_error(ZEUS_ERR_ARGUMENT, "zeus_pso_xchg_setup: bad arguments");
+  PsoXchg h;
+  memset(&h, 0, sizeof(h));
+  for (int q = 0; q < world; ++q) {
+    if (!bases[q]) return set_error(ZEUS_ERR_ARGUMENT, "zeus_pso_xchg_setup: null peer block");
+    h.cand[q] = (double*)bases[q];
+    h.flag[q] = (unsigned long long*)((char*)bases[q] + xchg_slots_bytes(d, world));
+  }
+  h.timeout = (unsigned*)((char*)block + xchg_slots_bytes(d, world) + (size_t)2 * world * 8);
+  h.rank = rank;
+  h.world = world;
+  cudaStream_t s = as_stream(stream);
+  int rc = check_cuda(cudaMemsetAsync(block, 0, xchg_desc_offset(d, world), s),
+                      "memset(pso exchange)");
+  if (!rc)
+    rc = check_cuda(cudaMemcpyAsync((char*)block + xchg_desc_offset(d, world), &h, sizeof(h),
+                                    cudaMemcpyHostToDevice, s),
+                    "upload(pso exchange descriptor)");
+  if (!rc) rc = check_cuda(cudaStreamSynchronize(s), "pso exchange setup");
+  return rc;
+}
+
+int zeus_pso_xchg_status(const void* block, int d, int world, unsigned* timed_out) {
+  if (!block || !timed_out || d < 1 || world < 1 || world > kXchgMaxRanks)
+    return set_error(ZEUS_ERR_ARGUMENT, "zeus_pso_xchg_status: bad arguments");
+  return check_cuda(cudaMemcpy(timed_out,
+                               (const char*)block + xchg_slots_bytes(d, world) +
+                                   (size_t)2 * world * 8,
+                               sizeof(unsigned), cudaMemcpyDeviceToHost),
+                    "read pso exchange status");
+}
+
+int zeus_pso_run_xchg(int obj, int d, int64_t n, int64_t i0, uint64_t seed, double lower,
+                      double upper, double w, double c1, double c2, int iter_pso, double* x,
+                      double* v, double* pbest, double* pval, int64_t ld, double* cand,
+                      double* gX, double* gbest, void* workspace, void* xchg_block, int world,
+                      unsigned long long seq0, void* stream) {
+  if (d < 1 || n < 0 || i0 < 0 || ld < n || ld < 1 || !(lower < upper) || iter_pso < 0 || !x ||
+      !v || !pbest || !pval || !cand || !gX || !gbest || !workspace || !xchg_block ||
+      world < 1 || world > kXchgMaxRanks || seq0 < 1 ||
+      (obj == ZEUS_OBJ_GOLDSTEIN_PRICE && d != 2))
+    return set_error(ZEUS_ERR_ARGUMENT, "zeus_pso_run_xchg: bad arguments");
+  const PsoXchg* xg = (const PsoXchg*)((char*)xchg_block + xchg_desc_offset(d, world));
+  const int rc = dispatch_objective<PsoRunLaunch>(obj, d, n, i0, seed, lower, upper, w, c1, c2,
+                                                  iter_pso, x, v, pbest, pval, ld, cand, gX,
+                                                  gbest, workspace, xg, seq0,
+                                                  as_stream(stream));
   if (rc == ZEUS_ERR_ARGUMENT) return set_error(rc, "unknown objective id %d", obj);
   return rc;
 }

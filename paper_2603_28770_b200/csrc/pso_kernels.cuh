@@ -121,9 +121,9 @@ __device__ __forceinline__ void finalize_body(int d, int nb, int64_t i0,
     }
   }
   __syncthreads();
-  const long long li = win - i0;
+  const long long li = win - i0;  // win < 0: empty shard, slot never selected
   for (int k = threadIdx.x; k < d; k += kPsoBlock) {
-    const double v = __ldcg(p + (int64_t)k * ld + li);
+    const double v = win < 0 ? 0.0 : __ldcg(p + (int64_t)k * ld + li);
     cand[2 + k] = v;
     if (gX) gX[k] = v;
   }
@@ -135,13 +135,96 @@ __global__ void __launch_bounds__(kPsoBlock)
   finalize_body(d, nb, i0, p, ld, blk_f, blk_i, cand, nullptr, nullptr);
 }
 
+// Cross-GPU barrier over peer memory (world > 1): every rank's exchange
+// block holds two phases of [world][d+2] candidate slots plus [world] u64
+// sequence flags; the descriptor below carries every rank's block as mapped
+// into this process (CUDA IPC over NVLink/NVSwitch; plain pointers when the
+// shards share a device).  The last block of a sweep stores this shard's
+// candidate into slot (phase, rank) of EVERY rank, fences at system scope,
+// release-stores seq into each rank's flag (phase, rank), then spins on its
+// own flags until all world slots carry seq and picks the global best from
+// its local copy in np.argmin order (pso.py:73-76) -- the per-sweep
+// all-gather + select done inside the sweep kernel, no NCCL launch, no host.
+// Two phases suffice: a rank can only publish sweep s+2 (same phase as s)
+// after every rank published s+1, i.e. after every rank finished reading s.
+constexpr int kXchgMaxRanks = 8;
+struct PsoXchg {
+  double* cand[kXchgMaxRanks];              // rank q's slots [2][world][d+2]
+  unsigned long long* flag[kXchgMaxRanks];  // rank q's flags [2][world]
+  unsigned* timeout;                        // this rank's: set if a peer never arrived
+  int rank, world;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __noinline__ void xchg_barrier(const PsoXchg* __restrict__ xg, unsigned long long seq,
+                                          int d, const double* cand, double* gX,
+                                          double* gbest) {
+  __shared__ int win;
+  const int W = xg->world, r = xg->rank, ph = (int)(seq & 1), stride = d + 2;
+  for (int e = threadIdx.x; e < W * stride; e += kPsoBlock) {
+    const int q = e / stride, k = e - q * stride;
+    xg->cand[q][(int64_t)(ph * W + r) * stride + k] = __ldcg(cand + k);
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < W) {
+    st_release_sys(xg->flag[threadIdx.x] + ph * W + r, seq);
+    const unsigned long long* f = xg->flag[r] + ph * W + threadIdx.x;
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(f) != seq) {
+      __nanosleep(128);
+      if (global_ns() - t0 > 20000000000ull) {  // 20 s: a peer died; report, don't hang
+        atomicExch(xg->timeout, 1u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  const double* mine = xg->cand[r] + (int64_t)ph * W * stride;
+  if (threadIdx.x == 0) {
+    double bf = 0.0;
+    long long bi = -1;
+    int bc = 0;
+    for (int q = 0; q < W; ++q) {
+      const double f = __ldcv(mine + (int64_t)q * stride);
+      const long long idx = (long long)__ldcv(mine + (int64_t)q * stride + 1);
+      if (argmin_better(f, idx, bf, bi)) {
+        bf = f;
+        bi = idx;
+        bc = q;
+      }
+    }
+    win = bc;
+    gbest[0] = bf;
+    gbest[1] = (double)bi;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < d; k += kPsoBlock)
+    gX[k] = __ldcv(mine + (int64_t)win * stride + 2 + k);
+}
+
 // Fused barrier (`done` != nullptr): the last block to finish reduces every
-// block's partial into the candidate (and, for one shard, the global best),
-// so a sweep is one launch.  Every block's writes are fenced before its ticket.
+// block's partial into the candidate (and, for one shard, the global best;
+// with `xg`, the global best over every rank's shard via xchg_barrier), so a
+// sweep is one launch.  Every block's writes are fenced before its ticket.
 __device__ __forceinline__ void fused_finalize(unsigned* done, int d, int64_t i0, const double* p,
                                                int64_t ld, const double* blk_f,
                                                const long long* blk_i, double* cand, double* gX,
-                                               double* gbest) {
+                                               double* gbest, const PsoXchg* xg,
+                                               unsigned long long seq) {
   __shared__ bool last;
   __threadfence();
   __syncthreads();
@@ -149,7 +232,13 @@ __device__ __forceinline__ void fused_finalize(unsigned* done, int d, int64_t i0
   __syncthreads();
   if (last) {
     __threadfence();
-    finalize_body(d, (int)gridDim.x, i0, p, ld, blk_f, blk_i, cand, gX, gbest);
+    if (xg) {
+      finalize_body(d, (int)gridDim.x, i0, p, ld, blk_f, blk_i, cand, nullptr, nullptr);
+      __syncthreads();
+      xchg_barrier(xg, seq, d, cand, gX, gbest);
+    } else {
+      finalize_body(d, (int)gridDim.x, i0, p, ld, blk_f, blk_i, cand, gX, gbest);
+    }
     if (threadIdx.x == 0) *done = 0u;  // ready for the next launch
   }
 }
@@ -162,7 +251,8 @@ __global__ void __launch_bounds__(kPsoBlock)
                     double vlow, double vrange, double* __restrict__ x, double* __restrict__ v,
                     double* __restrict__ p, double* __restrict__ pval, int64_t ld,
                     double* blk_f, long long* blk_i, unsigned* done, double* cand,
-                    double* gX_out, double* gbest_out) {
+                    double* gX_out, double* gbest_out, const PsoXchg* xg,
+                    unsigned long long seq) {
   const int64_t i = blockIdx.x * (int64_t)kPsoBlock + threadIdx.x;
   double bf = 0.0;
   long long bi = -1;
@@ -189,7 +279,7 @@ __global__ void __launch_bounds__(kPsoBlock)
   }
   if (done) {
     __syncthreads();  // block_argmin's shared scratch is reused by the finalize
-    fused_finalize(done, d, i0, p, ld, blk_f, blk_i, cand, gX_out, gbest_out);
+    fused_finalize(done, d, i0, p, ld, blk_f, blk_i, cand, gX_out, gbest_out, xg, seq);
   }
 }
 
@@ -201,7 +291,8 @@ __global__ void __launch_bounds__(kPsoBlock)
                      double c1, double c2, double* __restrict__ x, double* __restrict__ v,
                      double* __restrict__ p, double* __restrict__ pval, int64_t ld,
                      const double* gX, double* blk_f, long long* blk_i, unsigned* done,
-                     double* cand, double* gX_out, double* gbest_out) {
+                     double* cand, double* gX_out, double* gbest_out, const PsoXchg* xg,
+                     unsigned long long seq) {
   const int64_t i = blockIdx.x * (int64_t)kPsoBlock + threadIdx.x;
   double bf = 0.0;
   long long bi = -1;
@@ -236,7 +327,7 @@ __global__ void __launch_bounds__(kPsoBlock)
   }
   if (done) {
     __syncthreads();  // block_argmin's shared scratch is reused by the finalize
-    fused_finalize(done, d, i0, p, ld, blk_f, blk_i, cand, gX_out, gbest_out);
+    fused_finalize(done, d, i0, p, ld, blk_f, blk_i, cand, gX_out, gbest_out, xg, seq);
   }
 }
 

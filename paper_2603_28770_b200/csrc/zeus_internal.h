@@ -21,5 +21,7 @@ inline int check_launch(const char* what) { return check_cuda(cudaGetLastError()
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int current_sm_count();
+// byte offset of the PsoXchg descriptor inside a rank's exchange block (pso.cu)
+size_t xchg_desc_offset(int d, int world);
 
 }  // namespace zeus

@@ -206,6 +206,21 @@ def reduce_best(outcomes: Sequence[BfgsOutcome]) -> tuple[BfgsOutcome, int]:
     return best, best_index
 
 
+def _peer_exchange(process_group, world: int) -> bool:
+    """Fuse the multi-GPU PSO barrier into the sweep kernels (peer-memory
+    exchange) when the ranks' devices can map each other: NCCL groups of at
+    most 8 ranks.  ZEUS_PSO_EXCHANGE=collective forces the all-gather path,
+    =peer forces the exchange (e.g. gloo ranks sharing one GPU)."""
+    import os
+
+    mode = os.environ.get("ZEUS_PSO_EXCHANGE", "auto")
+    if mode == "collective" or world > 8:
+        return False
+    if mode == "peer":
+        return True
+    return not engine._host_backend(process_group)
+
+
 def _dist_world(process_group):
     if not torch.distributed.is_available() or not torch.distributed.is_initialized():
         return 0, 1
@@ -266,13 +281,20 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
 
     # ---- PSO phase (driver.py:236-241)
     pso_best = math.nan
+    xchg = None
     if starts is None:
         shard = engine.SwarmShard(obj, d, max(n, 1), lo, cfg.seed, dev)
         lower, upper = cfg.range
-        if world == 1 and isinstance(obj, int):
+        if world == 1:
             # one GPU: the barrier is the shard's own candidate -> fused sweeps
             shard.run_local(lower, upper, cfg.pso.w, cfg.pso.c1_pso, cfg.pso.c2_pso,
                             cfg.iter_pso)
+        elif _peer_exchange(process_group, world):
+            # several GPUs: the barrier is fused into every sweep launch as a
+            # peer-memory exchange of the shard candidates (no NCCL per sweep)
+            xchg = engine.PsoExchange.get(process_group, dev, d)
+            shard.run_xchg(xchg, n, lower, upper, cfg.pso.w, cfg.pso.c1_pso, cfg.pso.c2_pso,
+                           cfg.iter_pso)
         else:
             barrier = (engine.local_barrier if world == 1 else
                        engine.make_dist_barrier(process_group))
@@ -380,6 +402,8 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
     best_host = best_dev.cpu().numpy()  # (world > 1: every rank's [f, idx])
     sh = spack.cpu().numpy()
     stream.synchronize()
+    if xchg is not None:
+        xchg.check()
     device_time = ev_start.elapsed_time(ev_end) / 1e3
     fnp, inp = fh.numpy(), ih.numpy()
     x_host = fnp[:, :d]

@@ -167,18 +167,41 @@ class SwarmShard:
         LAUNCHES[0] += 2
         self.sweeps_done += 1
 
+    def _fused(self, n: int, lower: float, upper: float, w: float, c1: float, c2: float,
+               iter_pso: int, xg: "PsoExchange | None") -> None:
+        L = _capi.lib()
+        common = (int(n), self.i0, self.seed, float(lower), float(upper), float(w), float(c1),
+                  float(c2), int(iter_pso), self.x.data_ptr(), self.v.data_ptr(),
+                  self.p.data_ptr(), self.pval.data_ptr(), self.n, self.cand.data_ptr(),
+                  self.gX.data_ptr(), self.gbest.data_ptr(), self.ws.data_ptr())
+        xargs = (xg.block, xg.world, xg.seq) if xg is not None else (None, 1, 1)
+        if not isinstance(self.obj, int):
+            self.obj.bind(self._stream())
+            _capi.check(L.zeus_user_pso_run(self.obj.handle, *common, *xargs, self._stream()),
+                        "pso_run (user)")
+        elif xg is not None:
+            _capi.check(L.zeus_pso_run_xchg(self.obj, self.d, *common, *xargs, self._stream()),
+                        "pso_run_xchg")
+        else:
+            _capi.check(L.zeus_pso_run(self.obj, self.d, *common, self._stream()), "pso_run")
+        if xg is not None:
+            xg.seq += int(iter_pso) + 1
+        LAUNCHES[0] += 1 + int(iter_pso)
+        self.sweeps_done = int(iter_pso)
+
     def run_local(self, lower: float, upper: float, w: float, c1: float, c2: float,
                   iter_pso: int) -> None:
         """init + iter_pso sweeps + the barrier after each, when this shard is
         the whole swarm (one GPU): one fused launch per sweep (zeus_pso_run)."""
-        _capi.check(_capi.lib().zeus_pso_run(
-            self.obj, self.d, self.n, self.i0, self.seed, float(lower), float(upper), float(w),
-            float(c1), float(c2), int(iter_pso), self.x.data_ptr(), self.v.data_ptr(),
-            self.p.data_ptr(), self.pval.data_ptr(), self.n, self.cand.data_ptr(),
-            self.gX.data_ptr(), self.gbest.data_ptr(), self.ws.data_ptr(), self._stream()),
-            "pso_run")
-        LAUNCHES[0] += 1 + int(iter_pso)
-        self.sweeps_done = int(iter_pso)
+        self._fused(self.n, lower, upper, w, c1, c2, iter_pso, None)
+
+    def run_xchg(self, xg: "PsoExchange", n: int, lower: float, upper: float, w: float,
+                 c1: float, c2: float, iter_pso: int) -> None:
+        """init + iter_pso sweeps of this rank's shard (n real starts, may be
+        0) with the cross-GPU barrier fused into every launch (peer-memory
+        exchange, zeus_pso_run_xchg): same results as init/sweep + an
+        all-gather + select, without a collective launch per sweep."""
+        self._fused(n, lower, upper, w, c1, c2, iter_pso, xg)
 
     def select(self, cands: torch.Tensor, ncand: int) -> None:
         """Global best across shard candidates (np.argmin order, pso.py:73-76)."""
@@ -297,6 +320,96 @@ class StopBlock:
                         "stop block reset")
             stream.synchronize()
         dist.barrier(group=group)
+
+
+class PsoExchange:
+    """The per-sweep global-best exchange of a multi-GPU PSO phase, done over
+    peer memory inside the sweep kernels (csrc/pso_kernels.cuh xchg_barrier;
+    the reference's per-sweep reduction across shards, pso.py:73-76).  Every
+    rank allocates its exchange block (own cudaMalloc), the IPC handles are
+    all-gathered once, each rank maps its peers' blocks (NVLink/NVSwitch peer
+    access) and uploads the descriptor.  ``seq`` numbers the exchanges; all
+    ranks advance it identically (iter_pso + 1 per PSO phase).  One exchange
+    per (group, device, d), kept for the life of the process."""
+
+    _cache: dict = {}
+
+    def __init__(self, block: int, d: int, rank: int, world: int, opened=()):
+        self.block, self.d, self.rank, self.world = block, d, rank, world
+        self.opened = list(opened)
+        self.seq = 1
+
+    @classmethod
+    def get(cls, group, device, d: int) -> "PsoExchange":
+        import ctypes
+
+        import torch.distributed as dist
+
+        key = (id(group), device.index, d)
+        xg = cls._cache.get(key)
+        if xg is not None:
+            return xg
+        L = _capi.lib()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        nbytes = L.zeus_pso_xchg_bytes(d, world)
+        if nbytes == 0:
+            raise ValueError(f"peer-memory PSO exchange supports 1..8 ranks, not {world}")
+        handle = ctypes.create_string_buffer(64)
+        mine = ctypes.c_void_p()
+        _capi.check(L.zeus_ipc_alloc(nbytes, ctypes.byref(mine), handle), "pso exchange alloc")
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(handle.raw), group=group)
+        bases, opened = [], []
+        for q in range(world):
+            if q == rank:
+                bases.append(int(mine.value))
+                continue
+            ptr = ctypes.c_void_p()
+            _capi.check(L.zeus_ipc_open(handles[q], ctypes.byref(ptr)), "pso exchange open")
+            bases.append(int(ptr.value))
+            opened.append(int(ptr.value))
+        xg = cls(int(mine.value), d, rank, world, opened)
+        xg._setup(bases, device)
+        dist.barrier(group=group)  # every block zeroed before any rank publishes
+        cls._cache[key] = xg
+        return xg
+
+    @classmethod
+    def emulated(cls, device, d: int, world: int) -> list:
+        """``world`` exchanges on ONE device in one process (shards launched
+        on separate streams): the kernel protocol without IPC, for tests."""
+        import ctypes
+
+        L = _capi.lib()
+        nbytes = L.zeus_pso_xchg_bytes(d, world)
+        blocks = []
+        for _ in range(world):
+            ptr, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+            _capi.check(L.zeus_ipc_alloc(nbytes, ctypes.byref(ptr), handle), "exchange alloc")
+            blocks.append(int(ptr.value))
+        out = [cls(blocks[r], d, r, world) for r in range(world)]
+        for xg in out:
+            xg._setup(blocks, device)
+        return out
+
+    def _setup(self, bases, device) -> None:
+        import ctypes
+
+        arr = (ctypes.c_void_p * self.world)(*bases)
+        _capi.check(_capi.lib().zeus_pso_xchg_setup(self.block, self.d, self.rank, self.world,
+                                                    arr, _device.stream_ptr(device)),
+                    "pso exchange setup")
+
+    def check(self) -> None:
+        """Raise if a peer never arrived at an exchange (the kernel's 20 s
+        bound; the swarm results of that call are invalid)."""
+        import ctypes
+
+        flag = ctypes.c_uint(0)
+        _capi.check(_capi.lib().zeus_pso_xchg_status(self.block, self.d, self.world,
+                                                     ctypes.byref(flag)), "pso exchange status")
+        if flag.value:
+            raise RuntimeError("multi-GPU PSO exchange timed out: a peer rank did not arrive")
 
 
 def resolve_minloc(pairs) -> int:

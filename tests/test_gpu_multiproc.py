@@ -5,6 +5,8 @@ two processes on one GPU over gloo (the round's GPU box has one B200; on an
 * start sharding: per_run / best / tallies of a 2-rank run are bit-identical
   to the 1-process run (starts depend only on (seed, global
   index), the per-sweep barrier is an all-gather + np.argmin min-loc);
+* the same with the per-sweep barrier fused into the sweep kernels as a
+  peer-memory exchange over CUDA IPC (ZEUS_PSO_EXCHANGE=peer);
 * the cross-process early-stop block (driver.py:137-202: one counter and flag
   for the whole pool): a convergence counted in one process stops the other
   process's starts, through CUDA IPC-mapped device memory and system-scope
@@ -31,7 +33,7 @@ def _free_port():
 
 
 def _cfg(z, case):
-    if case == "shard":
+    if case in ("shard", "shard_peer"):
         return z.rastrigin, z.ZeusConfig(N=4099, dim=10, range=(-5.12, 5.12), iter_pso=5,
                                          iter_bfgs=2000, seed=11, deterministic=True)
     return z.rastrigin, z.ZeusConfig(N=20000, dim=2, range=(-5.12, 5.12), iter_pso=2,
@@ -43,6 +45,8 @@ def _worker(rank, world, port, q, case):
     os.environ["MASTER_PORT"] = str(port)
     import torch.distributed as dist
 
+    if case == "shard_peer":
+        os.environ["ZEUS_PSO_EXCHANGE"] = "peer"  # barrier fused into the sweeps over IPC
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
@@ -99,10 +103,14 @@ def _run(case, world=2):
     return out
 
 
-def test_two_process_run_is_bit_identical_to_one(z):
+@pytest.mark.parametrize("case", ["shard", "shard_peer"])
+def test_two_process_run_is_bit_identical_to_one(z, case):
+    """`shard_peer`: the per-sweep barrier runs inside the sweep kernels as a
+    peer-memory exchange between the two processes (IPC-mapped blocks,
+    system-scope release/acquire flags) instead of the all-gather."""
     fn, cfg = _cfg(z, "shard")
     one = z.zeus_run(fn, cfg)
-    for rank, x, f, s, k, gn, bf, conv, psob in _run("shard"):
+    for rank, x, f, s, k, gn, bf, conv, psob in _run(case):
         assert np.array_equal(x, one.per_run.x_final), rank
         assert np.array_equal(f, one.per_run.f_final, equal_nan=True)
         assert np.array_equal(s, one.per_run.status_codes)

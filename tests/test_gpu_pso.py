@@ -171,3 +171,44 @@ def test_fused_pso_run_matches_per_sweep_barriers(name, d, n, sweeps):
         engine.local_barrier(b)
     for t in ("x", "v", "p", "pval", "gX", "gbest", "cand"):
         assert torch.equal(getattr(a, t), getattr(b, t)), t
+
+
+@pytest.mark.parametrize("name,d,n,world,sweeps", [("rastrigin", 10, 5000, 2, 6),
+                                                   ("rastrigin", 10, 65536, 8, 20),
+                                                   ("rosenbrock", 100, 3000, 3, 4),
+                                                   ("goldstein_price", 2, 5, 8, 3)])
+def test_peer_exchange_matches_single_swarm(name, d, n, world, sweeps):
+    """Multi-GPU PSO with the barrier fused into the sweep kernels as a
+    peer-memory exchange (zeus_pso_run_xchg), `world` shards emulated on one
+    device, each on its own stream so the ranks' kernels really wait on each
+    other: every shard's particles and every rank's barrier result equal the
+    single-swarm run bit for bit (n=5, world=8: three empty shards).  Run
+    twice through the same exchanges: the sequence numbers carry over."""
+    from paper_2603_28770_b200 import engine
+
+    dev = torch.device("cuda", 0)
+    lo, hi = BOXES[name]
+    one = engine.SwarmShard(OBJ[name], d, n, 0, 11, dev)
+    one.run_local(lo, hi, 0.5, 1.2, 1.5, sweeps)
+    xgs = engine.PsoExchange.emulated(dev, d, world)
+    streams = [torch.cuda.Stream(dev) for _ in range(world)]
+    for rep in range(2):
+        shards = []
+        torch.cuda.synchronize()
+        for r in range(world):
+            a, b = engine.shard_bounds(n, r, world)
+            s = engine.SwarmShard(OBJ[name], d, max(b - a, 1), a, 11, dev)
+            shards.append((s, a, b))
+        torch.cuda.synchronize()
+        for r, (s, a, b) in enumerate(shards):
+            with torch.cuda.stream(streams[r]):
+                s.run_xchg(xgs[r], b - a, lo, hi, 0.5, 1.2, 1.5, sweeps)
+        torch.cuda.synchronize()
+        for xg in xgs:
+            xg.check()
+            assert xg.seq == 1 + (rep + 1) * (sweeps + 1)
+        for s, a, b in shards:
+            assert torch.equal(s.gX, one.gX) and torch.equal(s.gbest, one.gbest)
+            for t in ("x", "v", "p"):
+                assert torch.equal(getattr(s, t)[:, :b - a], getattr(one, t)[:, a:b]), t
+            assert torch.equal(s.pval[:b - a], one.pval[a:b])

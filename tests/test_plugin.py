@@ -153,3 +153,38 @@ def test_cli_fit_demo(tmp_path, capsys):
     text = rep.read_text()
     assert text.startswith("model: falling_spectrum\nbins: 40\n") and "chi_square:" in text
     assert "of pulls within +-2" in capsys.readouterr().out
+
+
+@pytest.mark.gpu
+def test_plugin_fused_and_peer_exchange_pso(z):
+    """A user objective through the fused PSO launches, alone and with the
+    multi-GPU peer-memory exchange (3 shards emulated on one device, one
+    stream each): the same swarm as the registered objective's single run."""
+    import torch
+
+    from paper_2603_28770_b200 import engine
+
+    dev = torch.device("cuda", 0)
+    f = z.DeviceObjective(RASTRIGIN_SRC, dim=6, name="rastrigin_plugin")
+    n, sweeps = 3000, 5
+    ref = engine.SwarmShard(1, 6, n, 0, 9, dev)
+    ref.run_local(-5.12, 5.12, 0.5, 1.2, 1.5, sweeps)
+    one = engine.SwarmShard(f, 6, n, 0, 9, dev)
+    one.run_local(-5.12, 5.12, 0.5, 1.2, 1.5, sweeps)
+    for t in ("x", "v", "p", "pval", "gX", "gbest"):
+        assert torch.equal(getattr(one, t), getattr(ref, t)), t
+    xgs = engine.PsoExchange.emulated(dev, 6, 3)
+    streams = [torch.cuda.Stream(dev) for _ in range(3)]
+    shards = []
+    for r in range(3):
+        a, b = engine.shard_bounds(n, r, 3)
+        shards.append((engine.SwarmShard(f, 6, b - a, a, 9, dev), a, b))
+    torch.cuda.synchronize()
+    for r, (s, a, b) in enumerate(shards):
+        with torch.cuda.stream(streams[r]):
+            s.run_xchg(xgs[r], b - a, -5.12, 5.12, 0.5, 1.2, 1.5, sweeps)
+    torch.cuda.synchronize()
+    for (s, a, b), xg in zip(shards, xgs):
+        xg.check()
+        assert torch.equal(s.gX, ref.gX) and torch.equal(s.gbest, ref.gbest)
+        assert torch.equal(s.x, ref.x[:, a:b])

@@ -142,7 +142,7 @@ struct BfgsWarp {
   // bfgs_common.cuh); the pending lazy rank-2 update is applied first so the
   // record holds H_k itself.
   __device__ void promote(const BfgsArgs& A, long long s, int lane, double* hreg, bool pending,
-                          double aj, double bj, double f0, const double* acc, double gnorm,
+                          double aj, double bj, double f0, const double* acc, double gsq,
                           double ddir, int k, int ls_trials, int grads, int prev_trials) {
     const int d = A.d;
     unsigned long long slot = 0;
@@ -158,7 +158,7 @@ struct BfgsWarp {
       rec[5] = f0;
       rec[6] = acc[0];
       rec[7] = Obj::NACC > 1 ? acc[Obj::NACC - 1] : 0.0;
-      rec[8] = gnorm;
+      rec[8] = gsq;
       rec[9] = ddir;
     }
     for (int j = lane; j < d; j += 32) {
@@ -204,7 +204,7 @@ struct BfgsWarp {
     __syncwarp();
     double f0 = 0.0;
     int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
-    double gnorm = __longlong_as_double(0x7ff0000000000000LL);
+    double gsq = __longlong_as_double(0x7ff0000000000000LL);  // |g|^2 (|g| = inf: no gradient)
     double ddir = 0.0;
     bool pending = false;
 
@@ -218,7 +218,7 @@ struct BfgsWarp {
       f0 = rec[5];
       acc[0] = rec[6];
       if (Obj::NACC > 1) acc[Obj::NACC - 1] = rec[7];
-      gnorm = rec[8];
+      gsq = rec[8];
       ddir = rec[9];
       for (int j = lane; j < d; j += 32) {
         x[j] = rec[kCarryHead + j];
@@ -270,7 +270,7 @@ struct BfgsWarp {
         goto done;
       }
       const double gg = warp_sum(part);
-      gnorm = sqrt(gg);
+      gsq = gg;
       ddir = -gg;  // g . (-g)
       __syncwarp();
     }
@@ -278,7 +278,7 @@ struct BfgsWarp {
     PHASE(5);  // prologue: loads, H = I, f(x0), first gradient
   iterate:
     for (;;) {
-      if (gnorm < A.theta) {
+      if (gsq <= A.gsq_max) {  // |g| < theta (bfgs.py:118), no sqrt on the path
         status = ZEUS_CONVERGED;
         break;
       }
@@ -288,7 +288,7 @@ struct BfgsWarp {
       }
       if constexpr (DR > 0 && NH == 0) {
         if (A.k1 > 0 && k == A.k1) {  // straggler: hand over to the helper-warp kernel
-          promote(A, s, lane, hreg, pending, a_col[0], b_col[0], f0, acc, gnorm, ddir, k,
+          promote(A, s, lane, hreg, pending, a_col[0], b_col[0], f0, acc, gsq, ddir, k,
                   ls_trials, grads, prev_trials);
           return;
         }
@@ -361,8 +361,9 @@ struct BfgsWarp {
       // ---- fused pass over H: lazy rank-2 update, u = H dg, w = H g'
       double u_own[DR > 0 ? 1 : kMaxC], w_own[DR > 0 ? 1 : kMaxC];
       if constexpr (DR > 0) {
-        // straight-line over DR rows (row4 zero-padded past d); update by select
-        double u0 = 0.0, u1 = 0.0, w0 = 0.0, w1 = 0.0;
+        // straight-line over DR rows (row4 zero-padded past d: every load is
+        // issued up front), four accumulator chains of DR / 4
+        double uq[4] = {0.0, 0.0, 0.0, 0.0}, wq[4] = {0.0, 0.0, 0.0, 0.0};
         const double aj = a_col[0], bj = b_col[0];
 #pragma unroll
         for (int i = 0; i < DR; ++i) {
@@ -371,16 +372,11 @@ struct BfgsWarp {
           const double upd = fma(r1.x, aj, fma(r1.y, bj, hreg[i]));
           const double h = pending ? upd : hreg[i];
           hreg[i] = h;
-          if (i & 1) {
-            u1 = fma(h, r0.x, u1);
-            w1 = fma(h, r0.y, w1);
-          } else {
-            u0 = fma(h, r0.x, u0);
-            w0 = fma(h, r0.y, w0);
-          }
+          uq[i & 3] = fma(h, r0.x, uq[i & 3]);
+          wq[i & 3] = fma(h, r0.y, wq[i & 3]);
         }
-        u_own[0] = u0 + u1;
-        w_own[0] = w0 + w1;
+        u_own[0] = (uq[0] + uq[1]) + (uq[2] + uq[3]);
+        w_own[0] = (wq[0] + wq[1]) + (wq[2] + wq[3]);
       } else {
         for (int c = 0; c < C; ++c) {
           const int j = lane + 32 * c;
@@ -440,11 +436,10 @@ struct BfgsWarp {
           part[6] = fma(dxj, gj, part[6]);
           part[7] = fma(wj, gj, part[7]);
         }
-        warp_sum8(part);
+        warp_sum8<(DR > 0 && DR <= 16) ? 16 : 32>(part);
       }
       const double curv = part[1];
-      const double ndx = sqrt(part[2]), ndg = sqrt(part[3]);
-      pending = !(curv <= kCurvatureFloor * ndx * ndg);  // bfgs.py:69-71
+      pending = curvature_update(curv, part[2], part[3]);  // bfgs.py:69-71
       double pd = 0.0;
       __syncwarp();  // row4 (dx/u of the previous iteration) fully consumed
       {
@@ -488,8 +483,8 @@ struct BfgsWarp {
       f0 = f_new;
 #pragma unroll
       for (int a = 0; a < Obj::NACC; ++a) acc[a] = acc_new[a];
-      gnorm = sqrt(part[0]);
-      ddir = warp_sum(pd);  // np.dot(g, p) of the next line search
+      gsq = part[0];
+      ddir = warp_sum_n<(DR > 0 && DR <= 16) ? 16 : 32>(pd);  // np.dot(g, p) of the next line search
       PHASE(4);  // ddir reduction + swap
       ++k;
       __syncwarp();
@@ -504,7 +499,7 @@ struct BfgsWarp {
     for (int j = lane; j < d; j += 32) o.x_final[(int64_t)j * o.ld_out + s] = x[j];
     if (lane == 0) {
       o.f_final[s] = f0;
-      o.grad_norm[s] = gnorm;
+      o.grad_norm[s] = sqrt(gsq);
       o.iterations[s] = k;
       o.status[s] = (uint8_t)status;
       if (o.ls_trials) o.ls_trials[s] = ls_trials;
@@ -645,7 +640,7 @@ static inline int even(int v) { return (v + 1) & ~1; }
 
 static BfgsPlan bfgs_plan(int d, int nacc, int nterms, int iter_ls) {
   BfgsPlan P{};
-  P.dr = d <= 16 ? 16 : d <= 32 ? 32 : 0;
+  P.dr = d <= 12 ? 12 : d <= 16 ? 16 : d <= 32 ? 32 : 0;
   P.tstride = std::max(1, nterms) | 1;
   // sizes depend on d only (never on iter_ls), so the workspace query and the
   // launch always agree on where H lives
@@ -736,6 +731,7 @@ struct BfgsResumeLaunch {
     A.tstride = P.tstride;
     A.bmax = P.bmax;
     A.nalpha = P.nalpha;
+    if (P.dr == 12) return launch_helpers<Obj, 12, ZEUS_NH>(A, P, s);
     if (P.dr == 16) return launch_helpers<Obj, 16, ZEUS_NH>(A, P, s);
     if (P.dr == 32) return launch_helpers<Obj, 32, ZEUS_NH>(A, P, s);
     return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs resume: d=%d", A.d);
@@ -751,6 +747,7 @@ struct BfgsLaunch {
     A.tstride = P.tstride;
     A.bmax = P.bmax;
     A.nalpha = P.nalpha;
+    if (P.dr == 12) return launch_plan<Obj, 12>(A, P, s);
     if (P.dr == 16) return launch_plan<Obj, 16>(A, P, s);
     if (P.dr == 32) return launch_plan<Obj, 32>(A, P, s);
     if (P.smem_h) A.h_global = nullptr;
@@ -828,6 +825,7 @@ int zeus_bfgs(int obj, int d, int64_t n, const double* x0, int64_t ldx,
   A.x0 = x0;
   A.ldx = ldx;
   A.theta = P->theta;
+  A.gsq_max = gsq_max_for(P->theta);
   A.cap = P->iter_bfgs;
   A.iter_ls = P->iter_ls;
   A.c1 = P->c1_armijo;

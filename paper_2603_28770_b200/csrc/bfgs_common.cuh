@@ -19,6 +19,10 @@ struct BfgsArgs {
   const double* x0;
   int64_t ldx;
   double theta;
+  // largest double q with sqrt(q) < theta (sqrt is correctly rounded and
+  // monotone, so |g| < theta <=> |g|^2 <= gsq_max): the convergence test
+  // without a sqrt on the iteration's critical path (thread / warp tiers)
+  double gsq_max;
   int cap;
   int iter_ls;
   double c1, alpha0, shrink;
@@ -48,9 +52,25 @@ struct BfgsArgs {
 };
 
 // Carry record layout (doubles): [0] start index, [1] k, [2] ls_trials,
-// [3] grads, [4] prev_trials, [5] f0, [6..7] acc, [8] gnorm, [9] ddir,
+// [3] grads, [4] prev_trials, [5] f0, [6..7] acc, [8] |g|^2, [9] ddir,
 // then x[d], g[d], p[d], H[d][d] (row-major, the pending rank-2 update applied).
 constexpr int kCarryHead = 10;
+
+#ifndef __CUDACC_RTC__
+// host: BfgsArgs::gsq_max for theta (NaN / <= 0: never converges)
+inline double gsq_max_for(double theta) {
+  if (!(theta > 0.0)) return -1.0;
+  if (isinf(theta)) return 1.7976931348623157e308;
+  double q = theta * theta;
+  while (q > 0.0 && !(sqrt(q) < theta)) q = nextafter(q, 0.0);
+  for (;;) {
+    const double up = nextafter(q, 1.0 / 0.0);
+    if (!(sqrt(up) < theta)) break;
+    q = up;
+  }
+  return q;
+}
+#endif
 __host__ __device__ inline int carry_stride_for(int d) { return kCarryHead + 3 * d + d * d; }
 
 constexpr int kBfgsWarps = 4;
@@ -99,31 +119,46 @@ struct TrialX {
 // Sum of 8 values over a warp, identical in every lane: a transpose-reduce
 // (each level halves the values a lane carries: 4+2+1+1+1 shuffles) followed
 // by 8 broadcasts -- 17 double shuffles instead of 40 for 8 butterflies.
+// 8 warp sums at once by a transpose-reduce (7 shuffles + 8 broadcasts
+// instead of 40).  LANES = 16: only lanes 0..15 hold non-zero values (d <= 16
+// column owners), one butterfly level less.  Every lane receives all 8 sums.
+template <int LANES = 32>
 __device__ __forceinline__ void warp_sum8(double v[8]) {
+  static_assert(LANES == 32 || LANES == 16, "warp_sum8: 16 or 32 lanes");
+  constexpr int S = LANES / 2;  // first butterfly distance
   const int lane = threadIdx.x & 31;
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  const bool b4 = lane & S, b3 = lane & (S / 2), b2 = lane & (S / 4);
   double w4[4], w2[2];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const double send = b4 ? v[q] : v[q + 4];
     const double keep = b4 ? v[q + 4] : v[q];
-    w4[q] = keep + __shfl_xor_sync(kFull, send, 16);
+    w4[q] = keep + __shfl_xor_sync(kFull, send, S);
   }
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const double send = b3 ? w4[q] : w4[q + 2];
     const double keep = b3 ? w4[q + 2] : w4[q];
-    w2[q] = keep + __shfl_xor_sync(kFull, send, 8);
+    w2[q] = keep + __shfl_xor_sync(kFull, send, S / 2);
   }
-  double w1 = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(kFull, b2 ? w2[0] : w2[1], 4);
-  w1 += __shfl_xor_sync(kFull, w1, 2);
-  w1 += __shfl_xor_sync(kFull, w1, 1);
+  double w1 = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(kFull, b2 ? w2[0] : w2[1], S / 4);
+#pragma unroll
+  for (int o = S / 8; o > 0; o >>= 1) w1 += __shfl_xor_sync(kFull, w1, o);
   // lane l now holds value index b2 + 2 b3 + 4 b4
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const int src = ((q >> 2) & 1) << 4 | ((q >> 1) & 1) << 3 | (q & 1) << 2;
+    const int src = ((q >> 2) & 1) * S | ((q >> 1) & 1) * (S / 2) | (q & 1) * (S / 4);
     v[q] = __shfl_sync(kFull, w1, src);
   }
+}
+
+// Warp sum when only lanes 0..LANES-1 hold non-zero values; all lanes get it.
+template <int LANES>
+__device__ __forceinline__ double warp_sum_n(double v) {
+#pragma unroll
+  for (int o = LANES / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  if constexpr (LANES < 32) v = __shfl_sync(kFull, v, 0);
+  return v;
 }
 
 // Term pass of a batch: (trial b, term j) pairs q = b * nt + j are spread over
@@ -191,8 +226,10 @@ __device__ __forceinline__ double seq_fold(const double* row, int nt, double s) 
 #pragma unroll
     for (int j = 0; j < MAXT; ++j) v[j] = j < nt ? row[j] : 0.0;
 #pragma unroll
-    for (int j = 0; j < MAXT; ++j)
-      if (j < nt) s = s + v[j];
+    for (int j = 0; j < MAXT; ++j) {  // the add chain is nt long, not MAXT
+      if (j >= nt) break;
+      s = s + v[j];
+    }
   } else {
     for (int j = 0; j < nt; ++j) s = s + row[j];
   }

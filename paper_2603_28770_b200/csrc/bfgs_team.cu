@@ -184,7 +184,7 @@ struct BfgsTeam {
       f0 = rec[5];
 #pragma unroll
       for (int a = 0; a < Obj::NACC; ++a) acc[a] = rec[6 + a];
-      gnorm = rec[8];
+      gnorm = sqrt(rec[8]);  // the record carries |g|^2
       ddir = rec[9];
       if (primary) {
         x[col] = rec[kCarryHead + col];

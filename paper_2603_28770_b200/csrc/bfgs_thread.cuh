@@ -106,7 +106,7 @@ struct ThreadStart {
     double acc[NA];
     double f0 = 0.0;
     int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
-    double gnorm = __longlong_as_double(0x7ff0000000000000LL);
+    double gsq = __longlong_as_double(0x7ff0000000000000LL);  // |g|^2 (|g| = inf: no gradient)
     double ddir = 0.0;
 
 #pragma unroll
@@ -152,12 +152,12 @@ struct ThreadStart {
         p[j] = -gx[j];
         gg = fma(gx[j], gx[j], gg);
       }
-      gnorm = sqrt(gg);
+      gsq = gg;
       ddir = -gg;
     }
 
     for (;;) {
-      if (gnorm < A.theta) {
+      if (gsq <= A.gsq_max) {  // |g| < theta (bfgs.py:118)
         status = ZEUS_CONVERGED;
         break;
       }
@@ -166,7 +166,7 @@ struct ThreadStart {
         break;
       }
       if (A.k1 > 0 && k == A.k1) {  // straggler: hand over to the CTA-team resume kernel
-        promote(A, s, x, p, g, f0, acc, gnorm, ddir, k, ls_trials, grads, prev_trials);
+        promote(A, s, x, p, g, f0, acc, gsq, ddir, k, ls_trials, grads, prev_trials);
         return;
       }
       // ---- Armijo backtracking (linesearch.py:60-71), one trial at a time
@@ -257,7 +257,7 @@ struct ThreadStart {
         wg = fma(w[j], gn[j], wg);
       }
       (void)wg;
-      const bool upd = !(curv <= kCurvatureFloor * sqrt(dxdx) * sqrt(dgdg));  // bfgs.py:69-71
+      const bool upd = curvature_update(curv, dxdx, dgdg);  // bfgs.py:69-71
       double pd = 0.0;
       if (upd) {
         const double rho = 1.0 / curv;
@@ -295,7 +295,7 @@ struct ThreadStart {
       f0 = f_new;
 #pragma unroll
       for (int a = 0; a < NA; ++a) acc[a] = acc_new[a];
-      gnorm = sqrt(gg);
+      gsq = gg;
       ddir = pd;  // np.dot(g, p) of the next line search
       ++k;
       if (A.stop_flag && *(volatile int*)A.stop_flag) {
@@ -310,7 +310,7 @@ struct ThreadStart {
     for (int j = 0; j < D; ++j)
       if (j < d) o.x_final[(int64_t)j * o.ld_out + s] = x[j];
     o.f_final[s] = f0;
-    o.grad_norm[s] = gnorm;
+    o.grad_norm[s] = sqrt(gsq);
     o.iterations[s] = k;
     o.status[s] = (uint8_t)status;
     if (o.ls_trials) o.ls_trials[s] = ls_trials;
@@ -324,7 +324,7 @@ struct ThreadStart {
   // carry record (bfgs_common.cuh): H written in full, both triangles
   __device__ void promote(const BfgsArgs& A, long long s, const double (&x)[D + 1],
                           const double (&p)[D + 1], const double (&g)[D + 1], double f0,
-                          const double acc[NA], double gnorm, double ddir, int k, int ls_trials,
+                          const double acc[NA], double gsq, double ddir, int k, int ls_trials,
                           int grads, int prev_trials) const {
     const int d = A.d;
     const unsigned long long slot = atomicAdd(A.promo_count, 1ull);
@@ -337,7 +337,7 @@ struct ThreadStart {
     rec[5] = f0;
     rec[6] = acc[0];
     rec[7] = NA > 1 ? acc[NA - 1] : 0.0;
-    rec[8] = gnorm;
+    rec[8] = gsq;
     rec[9] = ddir;
 #pragma unroll
     for (int j = 0; j < D; ++j) {

@@ -367,6 +367,7 @@ int zeus_user_bfgs(void* handle, int64_t n, const double* x0, int64_t ldx,
   A.x0 = x0;
   A.ldx = ldx;
   A.theta = P->theta;
+  A.gsq_max = gsq_max_for(P->theta);
   A.cap = P->iter_bfgs;
   A.iter_ls = P->iter_ls;
   A.c1 = P->c1_armijo;

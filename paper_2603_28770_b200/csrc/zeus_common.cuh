@@ -26,6 +26,27 @@ namespace zeus {
 constexpr double kTwoPi = 2.0 * 3.141592653589793;  // objectives.py:30 (2.0*math.pi)
 constexpr double kE = 2.718281828459045;             // math.e
 constexpr double kCurvatureFloor = 1e-12;            // bfgs.py:40
+
+// The curvature guard of bfgs.py:69-71, update <=> !(curv <= floor*|dx|*|dg|)
+// with |dx| = sqrt(dxdx), |dg| = sqrt(dgdg), decided without the two square
+// roots whenever the squared comparison is clear by a margin far above its
+// rounding error (curv^2 vs floor^2 dxdx dgdg, all normal and finite); only
+// the near-tie (and under/overflow) case evaluates the reference expression.
+// Same decision as the reference expression for every input.
+__device__ __forceinline__ bool curvature_update(double curv, double dxdx, double dgdg) {
+  constexpr double kMin = 2.2250738585072014e-308, kMax = 1e300;
+  const double q = curv * curv;
+  const double t = (kCurvatureFloor * kCurvatureFloor) * dxdx;  // every partial normal
+  const double r = t * dgdg;
+  const bool normal = t >= kMin && t <= kMax && r >= kMin && r <= kMax && q >= kMin && q <= kMax;
+  // floor*|dx|*|dg| is finite and >= 0 for finite norms (NaN / inf fall through)
+  if (curv <= 0.0 && dxdx <= 1e300 && dgdg <= 1e300) return false;
+  if (normal) {
+    if (q > r * (1.0 + 1e-9)) return true;
+    if (q < r * (1.0 - 1e-9)) return false;
+  }
+  return !(curv <= kCurvatureFloor * sqrt(dxdx) * sqrt(dgdg));
+}
 constexpr unsigned kFull = 0xffffffffu;
 
 // ---------------------------------------------------------------------------

@@ -150,3 +150,23 @@ def test_validation(z):
         z.bfgs_run(z.rastrigin, [1.0], theta=1e-6, iter_bfgs=-1)
     with pytest.raises(NotImplementedError):
         z.bfgs_run(lambda x: x[0] * x[0], [1.0], theta=1e-6, iter_bfgs=10)
+
+
+def test_sqrt_free_convergence_and_guard_decisions(tmp_path):
+    """The iteration tests decided without square roots (|g|^2 <= gsq_max,
+    the squared curvature guard with its exact near-tie fallback) take the
+    reference's decisions for every input: millions of random, boundary,
+    ulp-neighbour, zero, inf and NaN cases on the device."""
+    import os
+    import subprocess
+
+    from paper_2603_28770_b200 import _capi
+
+    csrc = os.path.join(os.path.dirname(_capi.__file__), "csrc")
+    exe = tmp_path / "guard_check"
+    subprocess.run(["nvcc", "-O3", "-fmad=false", "-gencode", "arch=compute_100a,code=sm_100a",
+                    "-I", csrc, "-o", str(exe), os.path.join(csrc, "tools", "guard_check.cu")],
+                   check=True, capture_output=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr

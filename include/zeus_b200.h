@@ -232,7 +232,8 @@ int zeus_stop_block_reset(void *block, void *stream);
 /* ---- user objectives: the reference's generic-scalar user callables
  * (pkg/README.md:70-87, autodiff.py) as device source, compiled at run time
  * with NVRTC together with this library's PSO and thread-per-start BFGS
- * kernels.  Contract of `source`: csrc/user_objective.cuh.  1 <= d <= 16.
+ * kernels.  Contract of `source`: csrc/user_objective.cuh.  1 <= d <= 128
+ * (BFGS: thread per start for d <= 16, the warp-per-start kernel above).
  * include_dir: the csrc/ directory holding the kernel headers.  The handle
  * is bound to the CUDA context current at compile time. */
 int zeus_user_compile(const char *source, int d, const char *include_dir, void **handle);

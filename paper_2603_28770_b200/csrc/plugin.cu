@@ -14,18 +14,20 @@
 #include <cuda.h>
 #include <nvrtc.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
 #include <vector>
 
-#include "bfgs_common.cuh"
+#include "bfgs_plan.h"
 #include "zeus_internal.h"
 
 namespace zeus {
 namespace {
 
-constexpr int kUserMaxD = 16;
+constexpr int kUserMaxD = 128;
+constexpr int kUserThreadMaxD = 16;  // d <= 16: thread per start; above: warp per start
 constexpr int kPsoBlockU = 256;   // pso_kernels.cuh kPsoBlock
 constexpr int kThreadBlockU = 64; // bfgs_thread.cuh kThreadBlock
 constexpr size_t kUserWsHeader = 256;
@@ -36,7 +38,16 @@ struct UserPlugin {
              value = nullptr, gradient = nullptr, armijo = nullptr;
   CUdeviceptr data_sym = 0;
   int d = 0;
+  bool warp = false;  // bfgs = the warp-per-start kernel (d > kUserThreadMaxD)
+  BfgsPlan plan{};    // its sizing
 };
+
+// Sizing of the warp-per-start kernel for a user objective: one term with
+// d + 2 tangent slots (user_program.cuh); H in registers (DR = the plan's
+// bucket, d <= 32) or in the shared-memory slice (d <= 128 always fits one
+// warp per CTA).  The NVRTC instance uses the plan's DR.
+BfgsPlan user_warp_plan(int d) { return bfgs_plan(d, 1, 1, 0, d + 2); }
+int user_warp_dr(int d) { return user_warp_plan(d).dr; }
 
 // per-thread log of the last failed compile (zeus_user_compile_log)
 thread_local std::string g_log;
@@ -128,7 +139,12 @@ int zeus_user_compile(const char* source, int d, const char* include_dir, void**
   snprintf(iflag, sizeof iflag, "-I%s", include_dir);
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false",
                         "-lineinfo", dflag, iflag};
-  const std::string k_bfgs = "zeus::bfgs_thread_kernel<zeus::UserObj, " + std::to_string(d) + ">";
+  // ZEUS_USER_WARP=1: warp per start for every d (tests compare the two kernels)
+  const char* force = getenv("ZEUS_USER_WARP");
+  const bool warp = d > kUserThreadMaxD || (force && force[0] == '1');
+  const std::string k_bfgs =
+      warp ? "zeus::bfgs_warp_kernel<zeus::UserObj, " + std::to_string(user_warp_dr(d)) + ", 0>"
+           : "zeus::bfgs_thread_kernel<zeus::UserObj, " + std::to_string(d) + ">";
   const char* names[] = {"zeus::pso_init_kernel<zeus::UserObj>",
                          "zeus::pso_sweep_kernel<zeus::UserObj>", "zeus::pso_finalize_kernel",
                          k_bfgs.c_str(), "zeus::user_value_kernel",
@@ -165,8 +181,15 @@ int zeus_user_compile(const char* source, int d, const char* include_dir, void**
     if (!rc)
       rc = cu_check(drv().ModuleGetGlobal(&up->data_sym, &sym_n, up->mod, "_ZN4zeus14zeus_user_dataE"),
                     "cuModuleGetGlobal(zeus_user_data)");
+    up->warp = warp;
+    if (warp) {
+      up->plan = user_warp_plan(d);
+      if (!up->plan.smem_h && up->plan.dr == 0)
+        rc = set_error(ZEUS_ERR_UNSUPPORTED, "user objective d=%d: H does not fit in smem", d);
+    }
     if (!rc) {
-      const int smem = (int)(sizeof(double) * (size_t)(d * (d + 1) / 2) * kThreadBlockU);
+      const int smem = warp ? (int)up->plan.smem
+                            : (int)(sizeof(double) * (size_t)(d * (d + 1) / 2) * kThreadBlockU);
       rc = cu_check(drv().FuncSetAttribute(up->bfgs, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                                        smem),
                     "cuFuncSetAttribute");
@@ -380,20 +403,32 @@ int zeus_user_bfgs(void* handle, int64_t n, const double* x0, int64_t ldx,
   A.work = (unsigned long long*)workspace;
   int rc = cu_check(drv().MemsetD8Async((CUdeviceptr)workspace, 0, 8, s), "memset(work)");
   if (rc) return rc;
-  const int smem = (int)(sizeof(double) * (size_t)(up->d * (up->d + 1) / 2) * kThreadBlockU);
+  int block = kThreadBlockU, smem = 0;
+  if (up->warp) {  // warp per start: no promotion tiers (k1 = 0), H in smem
+    const BfgsPlan& Pl = up->plan;
+    A.warp_doubles = (int)Pl.warp_doubles;
+    A.ldh = Pl.ldh;
+    A.tstride = Pl.tstride;
+    A.bmax = Pl.bmax;
+    A.nalpha = Pl.nalpha;
+    block = Pl.wpb * 32;
+    smem = (int)Pl.smem;
+  } else {
+    smem = (int)(sizeof(double) * (size_t)(up->d * (up->d + 1) / 2) * kThreadBlockU);
+  }
   int per_sm = 0;
-  rc = cu_check(drv().Occupancy(&per_sm, up->bfgs, kThreadBlockU, smem),
-                "occupancy(user bfgs)");
+  rc = cu_check(drv().Occupancy(&per_sm, up->bfgs, block, smem), "occupancy(user bfgs)");
   if (rc) return rc;
   const int sms = current_sm_count();
   if (per_sm < 1 || sms < 1) return set_error(ZEUS_ERR_UNSUPPORTED, "user bfgs: does not fit");
   int64_t grid = (int64_t)per_sm * sms;
-  const int64_t need = (n + kThreadBlockU - 1) / kThreadBlockU;
+  const int64_t per_block = up->warp ? block / 32 : kThreadBlockU;
+  const int64_t need = (n + per_block - 1) / per_block;
   if (grid > need) grid = need;
   void* args[] = {&A};
-  return cu_check(drv().LaunchKernel(up->bfgs, (unsigned)grid, 1, 1, kThreadBlockU, 1, 1, smem, s,
-                                 args, nullptr),
-                  "bfgs_thread_kernel(user)");
+  return cu_check(drv().LaunchKernel(up->bfgs, (unsigned)grid, 1, 1, block, 1, 1, smem, s,
+                                     args, nullptr),
+                  up->warp ? "bfgs_warp_kernel(user)" : "bfgs_thread_kernel(user)");
 }
 
 }  // extern "C"

@@ -23,7 +23,7 @@ constexpr int kPsoBlock = 256;
 // Streaming accumulator: feeds coordinates in order, reproduces value_seq.
 // Generic accumulator (user objectives, d <= kStreamMax): buffers the
 // coordinates, evaluates Obj's sequential value at the end.
-constexpr int kStreamMax = 64;
+constexpr int kStreamMax = 128;
 template <class Obj>
 struct StreamAcc {
   double xs[kStreamMax];

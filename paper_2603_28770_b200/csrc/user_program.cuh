@@ -1,11 +1,13 @@
 // user_program.cuh -- the tail of a user objective's NVRTC program
 // (plugin.cu): adapts the user's `objective<T>(x, d, data, err)` to the
 // framework's objective interface (objectives.cuh) and pulls in the PSO and
-// thread-per-start BFGS kernels, which NVRTC then instantiates for UserObj.
+// thread-per-start (d <= 16) and warp-per-start (d > 16) BFGS kernels, which
+// NVRTC then instantiates for UserObj.
 // Compiled only by NVRTC, with -DZEUS_USER_D=<d> (the problem dimension, so
 // every per-coordinate array is sized exactly).
 #pragma once
 #include "bfgs_thread.cuh"
+#include "bfgs_warp.cuh"
 #include "pso_kernels.cuh"
 
 namespace zeus {
@@ -26,12 +28,16 @@ struct PlainX {
 
 // The whole objective is one "term"; its tangents are the d partials from d
 // seeded Dual passes (the reference's forward_gradient).  Domain errors come
-// back through the `oor` flag (kOorIsError): the BFGS kernel turns them into
-// the domain_error status at the old iterate, as bfgs.py does.
+// back through the `oor` flag (kOorIsError) for the thread-per-start kernel,
+// and through two extra tangent slots for the warp-per-start kernel (d > 16),
+// whose speculative batches must tell which trial raised: slot d = the
+// gradient (or the value) raised, slot d + 1 = the value raised (its term
+// value is then NaN).  Either way the BFGS kernel turns them into the
+// domain_error status at the old iterate, as bfgs.py does.
 struct UserObj {
   static constexpr int kId = 100;
   static constexpr int NACC = 1;
-  static constexpr int KT = ZEUS_USER_D;
+  static constexpr int KT = ZEUS_USER_D + 2;
   static constexpr bool kOorIsError = true;
   __host__ __device__ static int nterms(int) { return 1; }
   __device__ static double init(int, int) { return 0.0; }
@@ -42,14 +48,25 @@ struct UserObj {
   }
   template <class M, class X>
   __device__ static void term_tan(const X& x, int, int d, double t[1], double tan[KT], bool& oor) {
-    t[0] = objective<double>(x, d, zeus_user_data, oor);
+    bool ev = false, eg = false;
+    const double f = objective<double>(x, d, zeus_user_data, ev);
+    t[0] = ev ? __longlong_as_double(0x7ff8000000000000LL) : f;
 #pragma unroll 1
-    for (int k = 0; k < KT; ++k)
-      tan[k] = k < d ? objective<Dual>(SeedX<X>{x, k}, d, zeus_user_data, oor).d : 0.0;
+    for (int k = 0; k < KT - 2; ++k)
+      tan[k] = k < d ? objective<Dual>(SeedX<X>{x, k}, d, zeus_user_data, eg).d : 0.0;
+    tan[KT - 2] = tan[KT - 1] = 0.0;
+    tan[d] = (ev || eg) ? 1.0 : 0.0;
+    tan[d + 1] = ev ? 1.0 : 0.0;
+    oor = oor || ev || eg;
   }
   template <class TA>
-  __device__ static double grad_from_tan(const TA& tan, int i, int, const double*, bool&) {
+  __device__ static double grad_from_tan(const TA& tan, int i, int d, const double*, bool& err) {
+    if (tan(0, d) != 0.0) err = true;
     return tan(0, i);
+  }
+  template <class TA>
+  __device__ static bool value_error(const TA& tan, int d) {
+    return tan(0, d + 1) != 0.0;
   }
 };
 

@@ -22,8 +22,9 @@ together with the framework's own PSO and BFGS kernels
 (the last four take ``err`` and raise the reference's DomainError cases), and
 ``data`` is an optional constant array (``data=`` below).  Gradients are
 forward-mode: one seeded Dual pass per coordinate, like the reference's
-forward_gradient.  ``dim`` <= 16.  A DomainError anywhere in a BFGS run
-gives the ``domain_error`` status exactly where the reference would.
+forward_gradient.  ``dim`` <= 128 (BFGS: one thread per start up to 16,
+one warp per start above).  A DomainError anywhere in a BFGS run gives the
+``domain_error`` status exactly where the reference would.
 """
 
 from __future__ import annotations
@@ -39,7 +40,7 @@ from . import _capi
 
 __all__ = ["DeviceObjective", "MAX_DIM"]
 
-MAX_DIM = 16
+MAX_DIM = 128
 CSRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc")
 _CACHE: dict = {}  # (device, sha1(source), dim) -> handle
 
@@ -61,7 +62,8 @@ class DeviceObjective:
         self.__name__ = name
         self.device = _device.require_device(device)
         L = _capi.lib()
-        key = (self.device.index, hashlib.sha1(source.encode()).hexdigest(), self.dim)
+        key = (self.device.index, hashlib.sha1(source.encode()).hexdigest(), self.dim,
+               os.environ.get("ZEUS_USER_WARP", ""))
         handle = _CACHE.get(key)
         if handle is None:
             h = ctypes.c_void_p()

@@ -112,7 +112,7 @@ __device__ T objective(const X& x, int d, const double* data, bool& err) {
     with pytest.raises(ValueError, match="does not compile"):
         z.DeviceObjective("this is not C++", dim=2)
     with pytest.raises(ValueError):
-        z.DeviceObjective(src, dim=17)
+        z.DeviceObjective(src, dim=129)
     g = z.forward_gradient(f, [3.0, 4.0])        # d|x|/dx = x / |x|
     assert np.allclose(g, [0.6, 0.8], rtol=0, atol=1e-15)
     with pytest.raises(z.DomainError):
@@ -188,3 +188,60 @@ def test_plugin_fused_and_peer_exchange_pso(z):
         xg.check()
         assert torch.equal(s.gX, ref.gX) and torch.equal(s.gbest, ref.gbest)
         assert torch.equal(s.x, ref.x[:, a:b])
+
+
+SQRT_WELL_SRC = """
+template <class T, class X>
+__device__ T objective(const X& x, int d, const double* data, bool& err) {
+  // defined for x0 >= -1 only: trials that step past it raise DomainError
+  T s = -4.0 * zu::sqrt(x(0) + 1.0, err);
+  for (int i = 0; i < d; ++i) s = s + (x(i) - 0.5) * (x(i) - 0.5) - zu::cos(2.0 * x(i));
+  return s;
+}
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [24, 40, 100])
+def test_plugin_warp_kernel_matches_registered(z, d):
+    """d > 16: the user objective runs on the warp-per-start kernel (NVRTC
+    instance of bfgs_warp.cuh); restating Rastrigin it gives the registered
+    objective's swarm bit for bit and the same statuses / minimisers."""
+    f = z.DeviceObjective(RASTRIGIN_SRC, dim=d, name=f"rastrigin_plugin_{d}")
+    n = 256 if d < 100 else 64
+    cfg = z.ZeusConfig(N=n, dim=d, range=(-5.12, 5.12), iter_pso=3, iter_bfgs=1000, seed=4,
+                       deterministic=True)
+    a = z.zeus_run(f, cfg)
+    b = z.zeus_run(z.rastrigin, cfg)
+    assert a.pso_best_before_bfgs == b.pso_best_before_bfgs
+    pa, pb = a.per_run, b.per_run
+    assert_outcomes_close(pa.x_final, pa.f_final, pa.status_codes, pb.x_final, pb.f_final,
+                          pb.status_codes, f"plugin d={d} vs registered", pb.grad_norm)
+
+
+@pytest.mark.gpu
+def test_plugin_warp_kernel_domain_errors_match_thread_kernel(z, monkeypatch):
+    """The warp kernel's speculative line search reports a DomainError only
+    when the sequential search would reach the raising trial: on a function
+    with a domain edge, every start's status, iteration count and counters
+    equal the thread-per-start kernel's (which evaluates trials in order)."""
+    d = 8
+    rng = np.random.default_rng(2)
+    x0 = rng.uniform(-1.0, 2.0, size=(512, d))
+    x0[:, 0] = rng.uniform(-0.999, -0.5, size=512)   # close to the edge x0 = -1
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("ZEUS_USER_WARP", mode)
+        f = z.DeviceObjective(SQRT_WELL_SRC, dim=d, name=f"sqrt_well_{mode}")
+        cfg = z.ZeusConfig(N=512, dim=d, range=(-1.0, 2.0), iter_pso=0, iter_bfgs=500, seed=0,
+                           deterministic=True)
+        res[mode] = z.zeus_run(f, cfg, starts=x0)
+    t, w = res["0"], res["1"]
+    st_t, st_w = t.per_run.status_codes, w.per_run.status_codes
+    assert np.sum(st_t == 3) > 0                        # domain_error: the edge is hit
+    assert np.array_equal(st_t, st_w)
+    assert np.array_equal(t.per_run.iterations, w.per_run.iterations)
+    assert np.array_equal(t.stats.ls_trials, w.stats.ls_trials)
+    assert np.array_equal(t.stats.grad_evals, w.stats.grad_evals)
+    assert_outcomes_close(w.per_run.x_final, w.per_run.f_final, st_w, t.per_run.x_final,
+                          t.per_run.f_final, st_t, "warp vs thread kernel", t.per_run.grad_norm)

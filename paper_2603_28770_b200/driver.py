@@ -289,10 +289,10 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
             # one GPU: the barrier is the shard's own candidate -> fused sweeps
             shard.run_local(lower, upper, cfg.pso.w, cfg.pso.c1_pso, cfg.pso.c2_pso,
                             cfg.iter_pso)
-        elif _peer_exchange(process_group, world):
+        elif _peer_exchange(process_group, world) and \
+                (xchg := engine.PsoExchange.get(process_group, dev, d)) is not None:
             # several GPUs: the barrier is fused into every sweep launch as a
             # peer-memory exchange of the shard candidates (no NCCL per sweep)
-            xchg = engine.PsoExchange.get(process_group, dev, d)
             shard.run_xchg(xchg, n, lower, upper, cfg.pso.w, cfg.pso.c1_pso, cfg.pso.c2_pso,
                            cfg.iter_pso)
         else:

@@ -340,37 +340,58 @@ class PsoExchange:
         self.seq = 1
 
     @classmethod
-    def get(cls, group, device, d: int) -> "PsoExchange":
+    def get(cls, group, device, d: int) -> "PsoExchange | None":
+        """The group's exchange for dimension d, or None on EVERY rank when
+        any rank cannot map its peers' blocks (the caller then uses the
+        collective barrier; the decision is agreed, so no rank waits on an
+        exchange the others skip)."""
         import ctypes
+        import logging
 
         import torch.distributed as dist
 
         key = (id(group), device.index, d)
-        xg = cls._cache.get(key)
-        if xg is not None:
-            return xg
+        if key in cls._cache:
+            return cls._cache[key]
         L = _capi.lib()
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         nbytes = L.zeus_pso_xchg_bytes(d, world)
-        if nbytes == 0:
-            raise ValueError(f"peer-memory PSO exchange supports 1..8 ranks, not {world}")
         handle = ctypes.create_string_buffer(64)
         mine = ctypes.c_void_p()
-        _capi.check(L.zeus_ipc_alloc(nbytes, ctypes.byref(mine), handle), "pso exchange alloc")
+        ok = nbytes > 0 and L.zeus_ipc_alloc(nbytes, ctypes.byref(mine), handle) == 0
         handles = [None] * world
-        dist.all_gather_object(handles, bytes(handle.raw), group=group)
+        dist.all_gather_object(handles, bytes(handle.raw) if ok else None, group=group)
         bases, opened = [], []
+        ok = ok and all(h is not None for h in handles)
         for q in range(world):
+            if not ok:
+                break
             if q == rank:
                 bases.append(int(mine.value))
                 continue
             ptr = ctypes.c_void_p()
-            _capi.check(L.zeus_ipc_open(handles[q], ctypes.byref(ptr)), "pso exchange open")
+            if L.zeus_ipc_open(handles[q], ctypes.byref(ptr)) != 0:
+                ok = False
+                break
             bases.append(int(ptr.value))
             opened.append(int(ptr.value))
-        xg = cls(int(mine.value), d, rank, world, opened)
-        xg._setup(bases, device)
-        dist.barrier(group=group)  # every block zeroed before any rank publishes
+        xg = None
+        if ok:
+            xg = cls(int(mine.value), d, rank, world, opened)
+            ok = L.zeus_pso_xchg_setup(xg.block, d, rank, world,
+                                       (ctypes.c_void_p * world)(*bases),
+                                       _device.stream_ptr(device)) == 0
+        votes = [None] * world
+        dist.all_gather_object(votes, bool(ok), group=group)  # also: every block zeroed
+        if not all(votes):
+            for p in opened:
+                L.zeus_ipc_close(p, 0)
+            if mine.value:
+                L.zeus_ipc_close(mine.value, 1)
+            logging.getLogger(__name__).warning(
+                "peer-memory PSO exchange unavailable (%s); using the collective barrier",
+                L.zeus_last_error().decode(errors="replace") if not ok else "a peer rank failed")
+            xg = None
         cls._cache[key] = xg
         return xg
 

@@ -2,7 +2,8 @@
 # memcheck + racecheck + synccheck of every kernel family on small configs
 # (race detection): thread / warp / CTA-team tiers (d <= 16, with
 # promotions), warp kernel (d = 24), wide kernel W = 1 (d = 40, 50) and W = 2
-# (d = 70, 100), fused PSO, the early-stop protocol, a user plug-in.
+# (d = 70, 100), fused PSO, the early-stop protocol, user plug-ins (thread and
+# warp kernels), the multi-GPU PSO peer exchange (3 emulated ranks).
 mkdir -p gpurun_out
 cat > /tmp/san.py <<'PY'
 import sys; sys.path.insert(0, '.')
@@ -27,6 +28,26 @@ __device__ T objective(const X& x, int d, const double* data, bool& err) {
 }""", dim=3, data=[1.0, 2.0, 3.0])
 r = z.zeus_run(f, z.ZeusConfig(N=100, dim=3, range=(-2.0, 2.0), iter_pso=2, iter_bfgs=60, seed=2))
 print("plugin", r.converged_count, r.best.f_final)
+# user objective on the warp kernel (d > 16)
+f = z.DeviceObjective(f.source, dim=24, data=[1.0 + 0.1 * i for i in range(24)])
+r = z.zeus_run(f, z.ZeusConfig(N=8, dim=24, range=(-2.0, 2.0), iter_pso=2, iter_bfgs=60, seed=2))
+print("plugin d=24", r.converged_count, r.best.f_final)
+# multi-GPU PSO peer exchange, 3 ranks emulated on one device (one stream each)
+import torch
+from paper_2603_28770_b200 import engine
+dev = torch.device("cuda", 0)
+xgs = engine.PsoExchange.emulated(dev, 10, 3)
+streams = [torch.cuda.Stream(dev) for _ in range(3)]
+shards = []
+for q in range(3):
+    a, b = engine.shard_bounds(700, q, 3)
+    shards.append((engine.SwarmShard(1, 10, b - a, a, 5, dev), b - a))
+torch.cuda.synchronize()
+for q, (sh, nq) in enumerate(shards):
+    with torch.cuda.stream(streams[q]):
+        sh.run_xchg(xgs[q], nq, -5.12, 5.12, 0.5, 1.2, 1.5, 3)
+torch.cuda.synchronize()
+print("exchange", [float(sh.gbest[0]) for sh, _ in shards])
 PY
 for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san.py > gpurun_out/$tool.txt 2>&1

@@ -52,7 +52,11 @@ def _worker(rank, world, port, q):
         xs = torch.arange(lo, hi, dtype=torch.float64).repeat(d, 1) + 100 * torch.arange(d)[:, None]
         per = -(-N // world)
         gx = driver._gather_rows(xs, per, world, None)[:, :N]
-        q.put((rank, lo, hi, g.numpy().copy(), win, twin, ewin, nwin, gx.numpy().copy()))
+        # the peer-memory exchange setup is agreed: without device memory
+        # (this CPU box) every rank gets None and falls back to the collective
+        xg = engine.PsoExchange.get(None, torch.device("cpu"), d)
+        q.put((rank, lo, hi, g.numpy().copy(), win, twin, ewin, nwin, gx.numpy().copy(),
+               xg is None))
     finally:
         dist.destroy_process_group()
 
@@ -68,7 +72,7 @@ def test_two_rank_plumbing():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, lo0, hi0, g0, w0, t0, e0, n0, x0), (r1, lo1, hi1, g1, w1, t1, e1, n1, x1) = out
+    (r0, lo0, hi0, g0, w0, t0, e0, n0, x0, f0), (r1, lo1, hi1, g1, w1, t1, e1, n1, x1, f1) = out
     assert (lo0, hi0, lo1, hi1) == (0, 6, 6, 11)
     assert np.array_equal(g0, g1)                 # identical gathered candidates on every rank
     assert w0 == w1 == 7                          # rank 1's f=1.0 at global index 6+1
@@ -77,6 +81,7 @@ def test_two_rank_plumbing():
     assert n0 == n1 == 6                          # NaN wins like np.argmin
     want = np.arange(11)[None, :] + 100 * np.arange(3)[:, None]
     assert np.array_equal(x0, want) and np.array_equal(x1, want)
+    assert f0 and f1                              # exchange unavailable on both: fallback
 
 
 def test_resolve_minloc_matches_np_argmin():

@@ -392,15 +392,17 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
     ipack = torch.empty((m_rows, 4), dtype=torch.int32, device=dev)
     for c, t in enumerate((cols[2], cols[3], cols[4], cols[5])):
         ipack[:, c] = t
-    spack = torch.empty(5, dtype=torch.float64, device=dev)
+    # scalars in one small table: tallies[4], the PSO best f, every rank's [f, idx]
+    spack = torch.empty(5 + best_dev.numel(), dtype=torch.float64, device=dev)
     spack[0:4] = tallies
     spack[4] = gbest[0] if gbest is not None else math.nan
+    spack[5:] = best_dev
     fh = torch.empty(fpack.shape, dtype=torch.float64, pin_memory=True)
     ih = torch.empty(ipack.shape, dtype=torch.int32, pin_memory=True)
     fh.copy_(fpack, non_blocking=True)
     ih.copy_(ipack, non_blocking=True)
-    best_host = best_dev.cpu().numpy()  # (world > 1: every rank's [f, idx])
     sh = spack.cpu().numpy()
+    best_host = sh[5:]  # (world > 1: every rank's [f, idx])
     stream.synchronize()
     if xchg is not None:
         xchg.check()

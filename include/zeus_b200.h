@@ -220,6 +220,10 @@ int zeus_count_within(int d, int64_t n, const double *x, int64_t ldx, const doub
 int zeus_ipc_alloc(size_t bytes, void **block, unsigned char *handle);
 int zeus_ipc_open(const unsigned char *handle, void **block);
 int zeus_ipc_close(void *block, int owner);
+/* Let kernels on `device` access memory of `peer` (cudaDeviceEnablePeerAccess;
+ * already enabled is not an error): the single-process multi-GPU run maps its
+ * exchange and stop blocks this way instead of through IPC handles. */
+int zeus_enable_peer_access(int device, int peer);
 #define ZEUS_STOP_BLOCK_BYTES 64
 #define ZEUS_IPC_HANDLE_BYTES 64
 int zeus_stop_block_create(void **block, unsigned char *handle);

@@ -97,6 +97,7 @@ _SIGNATURES = {
     "zeus_ipc_alloc": (_int, [_sz, ctypes.POINTER(_vp), ctypes.c_char_p]),
     "zeus_ipc_open": (_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "zeus_ipc_close": (_int, [_vp, _int]),
+    "zeus_enable_peer_access": (_int, [_int, _int]),
     "zeus_stop_block_create": (_int, [ctypes.POINTER(_vp), ctypes.c_char_p]),
     "zeus_stop_block_open": (_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "zeus_stop_block_close": (_int, [_vp, _int]),

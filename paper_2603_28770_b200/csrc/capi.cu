@@ -326,6 +326,32 @@ int zeus_ipc_close(void* dptr, int owner) {
                : check_cuda(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
 }
 
+// Kernels running on `device` may then load / store / atomically update
+// memory of `peer` (NVLink / NVSwitch), as the single-process multi-GPU run
+// needs for its exchange and stop blocks.  device == peer is a no-op.
+int zeus_enable_peer_access(int device, int peer) {
+  if (device < 0 || peer < 0) return set_error(ZEUS_ERR_ARGUMENT, "zeus_enable_peer_access");
+  if (device == peer) return ZEUS_OK;
+  int can = 0;
+  int rc = check_cuda(cudaDeviceCanAccessPeer(&can, device, peer), "cudaDeviceCanAccessPeer");
+  if (rc) return rc;
+  if (!can)
+    return set_error(ZEUS_ERR_UNSUPPORTED, "device %d cannot access device %d", device, peer);
+  int cur = 0;
+  rc = check_cuda(cudaGetDevice(&cur), "cudaGetDevice");
+  if (rc) return rc;
+  rc = check_cuda(cudaSetDevice(device), "cudaSetDevice");
+  if (!rc) {
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled)
+      (void)cudaGetLastError();  // clear the sticky-free status
+    else
+      rc = check_cuda(e, "cudaDeviceEnablePeerAccess");
+  }
+  cudaSetDevice(cur);
+  return rc;
+}
+
 int zeus_stop_block_create(void** dptr, unsigned char* handle) {
   return zeus_ipc_alloc(ZEUS_STOP_BLOCK_BYTES, dptr, handle);
 }

@@ -239,9 +239,150 @@ def _gather_rows(t: torch.Tensor, per: int, world: int, group) -> torch.Tensor:
     return out.permute(1, 0, 2).reshape(*lead, world * per)
 
 
+def _zeus_run_devices(obj, cfg: ZeusConfig, devs, starts, within, t0) -> ZeusResult:
+    """zeus_run over several GPUs from ONE process (``devices=``): shard g of
+    G runs on devs[g] on a stream of its own.  The PSO barrier is
+    the peer-memory exchange inside the sweep kernels (blocks addressed
+    directly, peer access enabled between the devices), the early-stop
+    counter/flag (workers > 0) is one block on devs[0] reached by every
+    device, and the per-shard results are merged on the host in global start
+    order -- the same per-start results as one GPU.  Every
+    shard's PSO is enqueued before anything else, so no host call can wait on
+    a device that waits on a shard not yet launched."""
+    G = len(devs)
+    N, d = cfg.N, cfg.dim
+    required_c = N if cfg.deterministic else int(cfg.required_c)
+    early = required_c < N
+    device_stop = early and cfg.workers > 0
+    launches0 = engine.LAUNCHES[0]
+    if starts is not None:
+        pts = np.asarray(starts, dtype=np.float64)
+        if pts.shape != (N, d):
+            raise ValueError(f"starts must have shape ({N}, {d})")
+    stop = None
+    if device_stop:
+        blk = engine.StopBlock.local(devs)
+        blk.reset_now(devs[0])
+        stop = (blk.counter, blk.flag)
+    xgs = engine.PsoExchange.local(devs, d) if starts is None else None
+    sh = []
+    for g, dev in enumerate(devs):  # ---- phase 1: every shard's PSO (driver.py:236-241)
+        lo, hi = engine.shard_bounds(N, g, G)
+        n = hi - lo
+        # one stream per shard (after the device's pending work): shards that
+        # share a device must not queue behind each other's exchange waits
+        stream = torch.cuda.Stream(dev)
+        stream.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.device(dev), torch.cuda.stream(stream):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record(stream)
+            if starts is None:
+                shard = engine.SwarmShard(obj, d, max(n, 1), lo, cfg.seed, dev)
+                shard.run_xchg(xgs[g], n, cfg.range[0], cfg.range[1], cfg.pso.w,
+                               cfg.pso.c1_pso, cfg.pso.c2_pso, cfg.iter_pso)
+                x0, gbest = shard.x[:, :n], shard.gbest
+            else:
+                x0 = (_device.to_soa(pts[lo:hi], dev) if n > 0 else
+                      torch.empty((d, 0), device=dev, dtype=torch.float64))
+                shard, gbest = None, None
+            ev[1].record(stream)
+        sh.append(dict(dev=dev, lo=lo, n=n, stream=stream, ev=ev, shard=shard, x0=x0,
+                       gbest=gbest))
+    params = engine.bfgs_params(cfg.theta, cfg.iter_bfgs, cfg.ls)
+    L = _capi.lib()
+    for c in sh:  # ---- phase 2: BFGS, reduction, packing, D2H (all asynchronous)
+        dev, n, lo = c["dev"], c["n"], c["lo"]
+        with torch.cuda.device(dev), torch.cuda.stream(c["stream"]):
+            out = engine.BfgsBuffers.allocate(d, n, dev)
+            if n > 0:
+                x0 = c["x0"]
+                engine.run_bfgs(obj, x0.contiguous() if x0.stride(0) != x0.shape[1] else x0,
+                                params, out, dev, required_c=required_c, stop=stop)
+            c["ev"][2].record(c["stream"])
+            best = torch.empty(2, dtype=torch.float64, device=dev)
+            tallies = torch.zeros(4, dtype=torch.int64, device=dev)
+            cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            if n > 0:
+                ws = _device.workspace(L.zeus_argmin_workspace_bytes(n), dev)
+                _capi.check(L.zeus_reduce_best(n, lo, out.f_final.data_ptr(),
+                                               out.status.data_ptr(), best.data_ptr(),
+                                               tallies.data_ptr(), ws.data_ptr(),
+                                               _device.stream_ptr(dev)), "reduce_best")
+                engine.LAUNCHES[0] += 2
+                if within is not None:
+                    opt = torch.tensor([float(v) for v in within[0]], dtype=torch.float64,
+                                       device=dev)
+                    _capi.check(L.zeus_count_within(d, n, out.x_final.data_ptr(),
+                                                    out.x_final.shape[1], opt.data_ptr(),
+                                                    float(within[1]), cnt.data_ptr(),
+                                                    _device.stream_ptr(dev)), "count_within")
+                    engine.LAUNCHES[0] += 1
+            else:
+                best[0], best[1] = math.nan, -1.0
+            c["ev"][3].record(c["stream"])
+            fpack = torch.empty((n, d + 2), dtype=torch.float64, device=dev)
+            fpack[:, :d] = out.x_final[:, :n].t()
+            fpack[:, d] = out.f_final[:n]
+            fpack[:, d + 1] = out.grad_norm[:n]
+            ipack = torch.empty((n, 4), dtype=torch.int32, device=dev)
+            for k, t in enumerate((out.iterations, out.status, out.ls_trials, out.grad_evals)):
+                ipack[:, k] = t[:n]
+            spack = torch.empty(8, dtype=torch.float64, device=dev)
+            spack[0:4] = tallies
+            spack[4] = c["gbest"][0] if c["gbest"] is not None else math.nan
+            spack[5:7] = best
+            spack[7] = cnt[0]
+            c["fh"] = torch.empty(fpack.shape, dtype=torch.float64, pin_memory=True)
+            c["ih"] = torch.empty(ipack.shape, dtype=torch.int32, pin_memory=True)
+            c["sh"] = torch.empty(8, dtype=torch.float64, pin_memory=True)
+            c["fh"].copy_(fpack, non_blocking=True)
+            c["ih"].copy_(ipack, non_blocking=True)
+            c["sh"].copy_(spack, non_blocking=True)
+    for c in sh:
+        c["stream"].synchronize()
+    for xg in xgs or ():
+        xg.check()
+    fnp = np.concatenate([c["fh"].numpy() for c in sh])
+    inp = np.concatenate([c["ih"].numpy() for c in sh])
+    shs = np.stack([c["sh"].numpy() for c in sh])
+    x_host = fnp[:, :d]
+    f_h, gn_h = fnp[:, d], fnp[:, d + 1]
+    it_h, st_h, ls_h, ge_h = inp[:, 0], inp[:, 1].astype(np.uint8), inp[:, 2], inp[:, 3]
+    m = len(f_h)
+    converged_count = int(shs[:, 0].sum())
+    n_in = int(shs[:, 7].sum()) if within is not None else None
+    if early and not device_stop:
+        # sequential semantics (driver.py:205-217): cut after the required_c-th convergence
+        conv = np.flatnonzero(st_h == 0)
+        if len(conv) >= required_c:
+            m = int(conv[required_c - 1]) + 1
+        converged_count = int(np.count_nonzero(st_h[:m] == 0))
+        valid = (st_h[:m] != 3) & ~np.isnan(f_h[:m])
+        if not valid.any():
+            raise NoValidOptimumError("all runs ended in domain errors")
+        bidx = int(np.flatnonzero(valid)[np.argmin(f_h[:m][valid])])
+        if within is not None:
+            tgt = np.asarray([float(v) for v in within[0]], dtype=np.float64)
+            n_in = int(np.count_nonzero(np.linalg.norm(x_host[:m] - tgt, axis=1) < within[1]))
+    else:
+        bidx = engine.resolve_minloc(shs[:, 5:7].tolist())
+        if bidx < 0:
+            raise NoValidOptimumError("all runs ended in domain errors")
+    per_run = OutcomeList(x_host, f_h, gn_h, it_h, st_h, length=m)
+    span = lambda a, b: max(c["ev"][a].elapsed_time(c["ev"][b]) for c in sh) / 1e3
+    stats = RunStats(iterations=it_h[:m], ls_trials=ls_h[:m], grad_evals=ge_h[:m],
+                     status_counts={s: int(np.count_nonzero(st_h[:m] == k))
+                                    for k, s in enumerate(STATUSES)},
+                     pso_time=span(0, 1), bfgs_time=span(1, 2), reduce_time=span(2, 3),
+                     kernel_launches=engine.LAUNCHES[0] - launches0, n_within=n_in)
+    return ZeusResult(best=per_run[bidx], per_run=per_run, converged_count=converged_count,
+                      wall_time=time.perf_counter() - t0, pso_best_before_bfgs=float(shs[0, 4]),
+                      device_time=span(0, 3), stats=stats)
+
+
 def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
              process_group=None, starts: Optional[np.ndarray] = None,
-             gather: bool = True, within=None) -> ZeusResult:
+             gather: bool = True, within=None, devices=None) -> ZeusResult:
     """Run the full pipeline on registered objective ``f`` (driver.py:220-265).
 
     Extensions (keyword-only, defaults reproduce the reference):
@@ -254,6 +395,10 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
       within        (optimum, radius): count the starts whose final point lies
                     within radius of optimum on device (bench.py:131-141),
                     reported as stats.n_within (summed over ranks).
+      devices       several GPUs from THIS process: an int (the first n
+                    devices) or a sequence of device indices / torch devices
+                    (one start shard per entry).  Same per-start results as
+                    one GPU; no torch.distributed needed.
 
     Early stop: ``deterministic`` or ``required_c == N`` runs every start.
     ``workers == 0`` with ``required_c < N`` reproduces the reference's
@@ -266,6 +411,24 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
     """
     t0 = time.perf_counter()
     obj = objective_id(f, cfg.dim)
+    if devices is not None:
+        if isinstance(devices, int):
+            devices = list(range(devices))
+        devs = [d if isinstance(d, torch.device) else torch.device("cuda", int(d))
+                for d in devices]
+        if not devs or any(d.type != "cuda" for d in devs):
+            raise ValueError("devices: one or more CUDA devices")
+        if _dist_world(process_group)[1] > 1:
+            raise ValueError("devices= runs in one process; do not combine with a process group")
+        for d_ in devs:
+            _device.require_device(d_)
+        if len(devs) > 1:
+            if not isinstance(obj, int) and len({d_.index for d_ in devs}) > 1:
+                raise NotImplementedError(
+                    "a user objective is compiled for one device: run one process per GPU "
+                    "(torchrun) to use several GPUs")
+            return _zeus_run_devices(obj, cfg, devs, starts, within, t0)
+        device = devs[0]
     dev = _device.require_device(device)
     rank, world = _dist_world(process_group)
     N, d = cfg.N, cfg.dim

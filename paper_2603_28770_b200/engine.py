@@ -308,6 +308,34 @@ class StopBlock:
         cls._cache[key] = blk
         return blk
 
+    @classmethod
+    def local(cls, devices) -> "StopBlock":
+        """The stop block of a single-process multi-GPU run: 64 B on the
+        first device, reached from the others through peer access."""
+        import ctypes
+
+        key = ("local", tuple(int(v.index) for v in devices))
+        blk = cls._cache.get(key)
+        if blk is not None:
+            return blk
+        L = _capi.lib()
+        idx = sorted({int(v.index) for v in devices})
+        for a in idx:
+            _capi.check(L.zeus_enable_peer_access(a, int(devices[0].index)), "peer access")
+        ptr, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+        with torch.cuda.device(devices[0]):
+            _capi.check(L.zeus_stop_block_create(ctypes.byref(ptr), handle), "stop block create")
+        blk = cls(int(ptr.value), True)
+        cls._cache[key] = blk
+        return blk
+
+    def reset_now(self, device) -> None:
+        """Zero counter and flag before any shard launches (single process)."""
+        stream = torch.cuda.current_stream(device)
+        _capi.check(_capi.lib().zeus_stop_block_reset(self.ptr, stream.cuda_stream),
+                    "stop block reset")
+        stream.synchronize()
+
     def arm(self, group, device) -> None:
         """Zero counter and flag once no rank still runs a previous call's
         kernel, and before any rank launches the next one."""
@@ -396,22 +424,47 @@ class PsoExchange:
         return xg
 
     @classmethod
-    def emulated(cls, device, d: int, world: int) -> list:
-        """``world`` exchanges on ONE device in one process (shards launched
-        on separate streams): the kernel protocol without IPC, for tests."""
+    def local(cls, devices, d: int) -> list:
+        """One exchange per shard of a SINGLE-process multi-GPU run (one shard
+        per entry of ``devices``; a device may repeat, its shards then run on
+        separate streams): every block lives on its shard's device and is
+        addressed directly -- peer access enabled between every pair of
+        distinct devices, no IPC.  Cached per (devices, d)."""
         import ctypes
 
+        key = ("local", tuple(int(v.index) for v in devices), d)
+        if key in cls._cache:
+            return cls._cache[key]
         L = _capi.lib()
+        world = len(devices)
         nbytes = L.zeus_pso_xchg_bytes(d, world)
+        if nbytes == 0:
+            raise ValueError(f"the PSO exchange supports 1..8 shards, not {world}")
+        idx = sorted({int(v.index) for v in devices})
+        for a in idx:
+            for b in idx:
+                _capi.check(L.zeus_enable_peer_access(a, b), f"peer access {a} -> {b}")
         blocks = []
-        for _ in range(world):
+        for dev in devices:
             ptr, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
-            _capi.check(L.zeus_ipc_alloc(nbytes, ctypes.byref(ptr), handle), "exchange alloc")
+            with torch.cuda.device(dev):
+                _capi.check(L.zeus_ipc_alloc(nbytes, ctypes.byref(ptr), handle),
+                            "exchange alloc")
             blocks.append(int(ptr.value))
         out = [cls(blocks[r], d, r, world) for r in range(world)]
-        for xg in out:
-            xg._setup(blocks, device)
+        for xg, dev in zip(out, devices):
+            with torch.cuda.device(dev):
+                xg._setup(blocks, dev)
+        cls._cache[key] = out
         return out
+
+    @classmethod
+    def emulated(cls, device, d: int, world: int) -> list:
+        """``world`` fresh exchanges on ONE device (tests of the kernel
+        protocol: each shard on its own stream)."""
+        key = ("local", (int(device.index),) * world, d)
+        cls._cache.pop(key, None)
+        return cls.local([device] * world, d)
 
     def _setup(self, bases, device) -> None:
         import ctypes

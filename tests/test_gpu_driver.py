@@ -198,3 +198,47 @@ def test_full_size_wide_configs_properties(z, name, d, n, cap):
     assert np.array_equal(a.per_run.f_final, b.per_run.f_final, equal_nan=True)
     assert np.array_equal(a.per_run.iterations, b.per_run.iterations)
     assert np.array_equal(a.per_run.status_codes, b.per_run.status_codes)
+
+
+def test_devices_single_process_matches_one_gpu(z):
+    """zeus_run(devices=...) from one process: shards on separate streams (the
+    one GPU repeated here; distinct GPUs on a node), the PSO barrier inside
+    the sweep kernels over the exchange blocks -- per-start results, best,
+    PSO best and counts bit-identical to the one-GPU run, for the PSO path,
+    host-supplied starts and an empty shard (N < shards)."""
+    cfg = z.ZeusConfig(N=5000, dim=10, range=(-5.12, 5.12), iter_pso=6, iter_bfgs=2000, seed=9,
+                       deterministic=True)
+    one = z.zeus_run(z.rastrigin, cfg, within=([0.0] * 10, 0.5))
+    for devs in ([0, 0], [0, 0, 0]):
+        many = z.zeus_run(z.rastrigin, cfg, devices=devs, within=([0.0] * 10, 0.5))
+        a, b = one.per_run, many.per_run
+        assert len(b) == 5000
+        assert np.array_equal(a.x_final, b.x_final) and np.array_equal(a.status_codes, b.status_codes)
+        assert np.array_equal(a.f_final, b.f_final, equal_nan=True)
+        assert np.array_equal(a.iterations, b.iterations)
+        assert many.best == one.best and many.converged_count == one.converged_count
+        assert many.pso_best_before_bfgs == one.pso_best_before_bfgs
+        assert many.stats.n_within == one.stats.n_within
+    starts = np.random.default_rng(3).uniform(-5, 5, size=(3, 4))
+    c3 = z.ZeusConfig(N=3, dim=4, range=(-5.0, 5.0), iter_bfgs=500, deterministic=True)
+    r1 = z.zeus_run(z.rosenbrock, c3, starts=starts)
+    r8 = z.zeus_run(z.rosenbrock, c3, starts=starts, devices=[0] * 8)
+    assert np.array_equal(r1.per_run.x_final, r8.per_run.x_final) and r1.best == r8.best
+
+
+def test_devices_single_process_early_stop(z):
+    """required_c < N over several shards of one process: sequential
+    semantics (workers = 0) give the one-GPU prefix exactly; the device stop
+    protocol (workers > 0) stops every shard through the one shared block."""
+    seq = z.ZeusConfig(N=4000, dim=2, range=(-5.12, 5.12), iter_pso=2, iter_bfgs=1000,
+                       required_c=50, seed=5)
+    a = z.zeus_run(z.rastrigin, seq)
+    b = z.zeus_run(z.rastrigin, seq, devices=[0, 0])
+    assert len(a.per_run) == len(b.per_run) and a.best == b.best
+    assert np.array_equal(a.per_run.status_codes, b.per_run.status_codes)
+    par = z.ZeusConfig(N=20000, dim=2, range=(-5.12, 5.12), iter_pso=2, iter_bfgs=1000,
+                       required_c=100, workers=2, seed=5)
+    r = z.zeus_run(z.rastrigin, par, devices=[0, 0])
+    s = r.per_run.status_codes
+    assert len(s) == 20000 and r.converged_count >= 100
+    assert np.any(s[:10000] == 2) and np.any(s[10000:] == 2)   # both shards stopped

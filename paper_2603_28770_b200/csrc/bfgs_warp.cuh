@@ -276,9 +276,12 @@ struct BfgsWarp {
             __syncwarp();
           }
           double accb[Obj::NACC];
+          // Armijo threshold of this lane's trial, formed before the batch
+          // so its latency hides behind the term pass (same ops, same order)
+          const double thr = f0 + A.c1 * atab[lane] * ddir;
           const double fb = evalb(A, B, atab, d, TT, lane, accb);
           bool pass = false;
-          if (lane < B) pass = fb <= f0 + A.c1 * atab[lane] * ddir;  // NaN fails
+          if (lane < B) pass = fb <= thr;  // NaN fails
           const unsigned m = __ballot_sync(kFull, pass);
           if constexpr (Obj::kOorIsError) {
             // user objective: a trial whose value raised DomainError ends the

@@ -369,7 +369,10 @@ def _zeus_run_devices(obj, cfg: ZeusConfig, devs, starts, within, t0) -> ZeusRes
         if bidx < 0:
             raise NoValidOptimumError("all runs ended in domain errors")
     per_run = OutcomeList(x_host, f_h, gn_h, it_h, st_h, length=m)
-    span = lambda a, b: max(c["ev"][a].elapsed_time(c["ev"][b]) for c in sh) / 1e3
+
+    def span(a: int, b: int) -> float:  # slowest shard between two of its events
+        return max(c["ev"][a].elapsed_time(c["ev"][b]) for c in sh) / 1e3
+
     stats = RunStats(iterations=it_h[:m], ls_trials=ls_h[:m], grad_evals=ge_h[:m],
                      status_counts={s: int(np.count_nonzero(st_h[:m] == k))
                                     for k, s in enumerate(STATUSES)},

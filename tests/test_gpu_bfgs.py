@@ -170,3 +170,70 @@ def test_sqrt_free_convergence_and_guard_decisions(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("name,d,n", [("rastrigin", 10, 2048), ("rosenbrock", 4, 1024),
+                                      ("ackley", 6, 1024), ("rastrigin", 24, 128)])
+@pytest.mark.parametrize("cap", [0, 1, 15, 16, 17, 47, 48, 49])
+def test_caps_at_the_tier_boundaries(oracle, name, d, n, cap):
+    """The small-d tiers hand a start over at k1t = 16 (thread -> warp) and
+    k1 = 48 (warp -> CTA team).  With the cap on either side of a hand-over
+    (and caps 0 / 1) every start ends converged (|g| < theta) or diverged at
+    exactly k = cap -- a start whose cap equals a hand-over iteration stops,
+    it is not handed over.  Against the oracle: caps 0 / 1 exactly (status,
+    k, gradient and trial counts); later caps for every start whose uncapped
+    run converges at the same iteration on both sides (iteration counts are
+    not gated in general: a rounding-level difference can flip one Armijo
+    decision and reroute a Rastrigin path): its status at this cap is then
+    fixed -- converged iff its uncapped k <= cap -- and both must show it."""
+    lo, hi = BOXES[name]
+    starts = oracle.pso(name, d, n, 5, lo, hi, 1).positions
+    ref = oracle.bfgs_batch(name, starts, iter_bfgs=cap)
+    dev = device_bfgs(name, starts, cap)
+    s, k, gn = dev["s"], dev["k"], dev["gn"]
+    assert set(np.unique(s)) <= {0, 1}
+    assert np.all(k[s == 1] == cap) and np.all(k <= cap)
+    assert np.array_equal(s == 0, gn < 1e-6)
+    if cap <= 1:
+        check(dev, ref.x_final, ref.f_final, ref.status, ref.iterations, f"{name} cap={cap}",
+              ref.grad_norm)
+        assert np.array_equal(k, ref.iterations) and np.array_equal(dev["ng"], ref.grad_evals)
+        assert np.array_equal(dev["ls"], ref.ls_trials)
+        return
+    full_ref = oracle.bfgs_batch(name, starts, iter_bfgs=2000)
+    full_dev = device_bfgs(name, starts, 2000)
+    same = (full_ref.status == 0) & (full_dev["s"] == 0) & (full_ref.iterations == full_dev["k"])
+    # (d > 16 folds f in tree order, not the reference's: more paths reroute)
+    assert same.mean() > (0.8 if d <= 16 else 0.4), same.mean()
+    want = np.where(full_ref.iterations <= cap, 0, 1)
+    assert np.array_equal(s[same], want[same]), np.flatnonzero(s[same] != want[same])[:10]
+    assert np.array_equal(ref.status[same], want[same])
+    assert np.array_equal(k[same], np.minimum(full_ref.iterations, cap)[same])
+
+
+def test_theta_and_line_search_extremes(oracle):
+    """theta so large every start converges at k = 0 (one gradient, no
+    trial); iter_ls = 1 (two trials at most: alpha0, then the shrunk step
+    taken whatever its value) against the oracle over the first iterations
+    (longer iter_ls = 1 Rastrigin runs are chaotic: near-full steps)."""
+    from paper_2603_28770_b200 import engine
+    from paper_2603_28770_b200.linesearch import LineSearchParams
+
+    lo, hi = BOXES["rastrigin"]
+    starts = oracle.pso("rastrigin", 10, 512, 7, lo, hi, 1).positions
+    dev = device_bfgs("rastrigin", starts, 100, theta=1e10)
+    assert np.all(dev["s"] == 0) and np.all(dev["k"] == 0) and np.all(dev["ls"] == 0)
+    assert np.all(dev["ng"] == 1)
+    d_ = torch.device("cuda", 0)
+    x0 = torch.from_numpy(np.ascontiguousarray(starts.T)).to(d_)
+    for cap in (1, 2, 3):
+        ref = oracle.bfgs_batch("rastrigin", starts, iter_bfgs=cap, iter_ls=1)
+        out = engine.BfgsBuffers.allocate(10, 512, d_)
+        engine.run_bfgs(1, x0, engine.bfgs_params(1e-6, cap, LineSearchParams(iter_ls=1)), out,
+                        d_)
+        got = dict(x=out.x_final.cpu().numpy().T, f=out.f_final.cpu().numpy(),
+                   s=out.status.cpu().numpy().astype(np.int64), k=out.iterations.cpu().numpy())
+        check(got, ref.x_final, ref.f_final, ref.status, ref.iterations, f"iter_ls=1 cap={cap}",
+              ref.grad_norm)
+        assert np.array_equal(out.ls_trials.cpu().numpy(), ref.ls_trials)
+        assert np.all(ref.ls_trials <= 2 * cap)

@@ -51,7 +51,7 @@ __device__ __forceinline__ Dual operator/(Dual a, double s) { return {a.r / s, a
 struct FastMath {
   __device__ static __forceinline__ double cos(double x, bool& oor) {
     oor |= !trig_in_range(x);
-    return sincos_fast(x).c;
+    return cos_fast(x);  // == sincos_fast(x).c, one polynomial chain
   }
   __device__ static __forceinline__ SinCos sincos(double x, bool& oor) {
     oor |= !trig_in_range(x);
@@ -69,7 +69,7 @@ struct PreciseMath {
 // Single-call policy (PSO, thread-sequential code): fast path, libm fallback.
 struct AutoMath {
   __device__ static __forceinline__ double cos(double x, bool&) {
-    return trig_in_range(x) ? sincos_fast(x).c : ::cos(x);
+    return trig_in_range(x) ? cos_fast(x) : ::cos(x);
   }
   __device__ static __forceinline__ SinCos sincos(double x, bool&) {
     if (trig_in_range(x)) return sincos_fast(x);

@@ -1,5 +1,6 @@
 // Device check of the sqrt-free BFGS tests (bfgs_common.cuh gsq_max_for,
-// zeus_common.cuh curvature_update) against the reference expressions;
+// zeus_common.cuh curvature_update) against the reference expressions, and
+// of the one-polynomial cos_fast against sincos_fast (zeus_trig.cuh);
 // built and run by tests/test_gpu_bfgs.py.
 #include <cstdio>
 #include <cmath>
@@ -12,6 +13,14 @@ __global__ void k(const double* c, const double* a, const double* b, int n, int*
   bool ref = !(c[i] <= kCurvatureFloor * sqrt(a[i]) * sqrt(b[i]));
   if (ref != curvature_update(c[i], a[i], b[i])) atomicAdd(bad, 1);
 }
+// cos_fast(x) == sincos_fast(x).c bit for bit
+__global__ void kc(const double* x, int n, int* bad) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double a = cos_fast(x[i]), b = sincos_fast(x[i]).c;
+  if (__double_as_longlong(a) != __double_as_longlong(b)) atomicAdd(bad, 1);
+}
+
 // |g| < theta <=> |g|^2 <= gsq_max_for(theta), checked with the device sqrt
 __global__ void kt(const double* q, int n, double theta, double qmax, int* bad) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -61,5 +70,22 @@ int main() {
     printf("theta %g: gsq_max %.17g, mismatches %d\n", theta, qm, hb);
     h2 += hb;
   }
-  return (h != 0 || h2 != 0);
+  // cos_fast vs sincos_fast: uniform over the fast range, small arguments,
+  // neighbourhoods of multiples of pi/4 (quadrant edges), tiny and signed zeros
+  std::vector<double> xs(n);
+  std::uniform_real_distribution<double> big(-1e5, 1e5), small(-10.0, 10.0), tiny(-1e-7, 1e-7);
+  for (int i = 0; i < n; ++i) {
+    const int m = i % 4;
+    if (m == 0) xs[i] = big(rng);
+    else if (m == 1) xs[i] = small(rng);
+    else if (m == 2) xs[i] = (double)((i / 4) % 20001 - 10000) * 0.7853981633974483 + tiny(rng);
+    else xs[i] = (i % 8 == 3) ? tiny(rng) : ((i % 16 == 7) ? -0.0 : 6.283185307179586 * small(rng));
+  }
+  cudaMemcpy(dc, xs.data(), n * 8, cudaMemcpyHostToDevice);
+  cudaMemset(bad, 0, 4);
+  kc<<<(n + 255) / 256, 256>>>(dc, n, bad);
+  int h3 = -1;
+  cudaMemcpy(&h3, bad, 4, cudaMemcpyDeviceToHost);
+  printf("cos_fast vs sincos_fast: %d mismatches of %d\n", h3, n);
+  return (h != 0 || h2 != 0 || h3 != 0);
 }

@@ -133,6 +133,66 @@ __host__ __device__ __forceinline__ SinCos sincos_fast(double x) {
   return out;
 }
 
+// cos alone, bit-identical to sincos_fast(x).c with ONE polynomial chain:
+// cos x is +-cos r (q even) or -+sin r (q odd), and the two double-double
+// kernels above share their shape -- head + leading correction (rh / 1 - z/2
+// with c3 S1 / w C1), a tail polynomial and a low-order term -- so the
+// parity of q selects the operands and constants of one evaluation, each
+// sum keeping its own kernel's association.  Half the FP64 work of the pair
+// for the value-only calls (line-search trials, PSO sweeps).
+__host__ __device__ __forceinline__ double cos_fast(double x) {
+#ifdef __CUDA_ARCH__
+  const double INV_PIO2 = kSinCosTab[0], PIO2_1 = kSinCosTab[1], PIO2_1T = kSinCosTab[2],
+               PIO2_1TT = kSinCosTab[3];
+  const double shifted = x * INV_PIO2 + 6755399441055744.0;
+  const double fn = shifted - 6755399441055744.0;
+  const int q = __double2loint(shifted) & 3;
+  const bool odd = q & 1;
+  const double K1 = odd ? kSinCosTab[4] : kSinCosTab[10], K2 = odd ? kSinCosTab[5] : kSinCosTab[11],
+               K3 = odd ? kSinCosTab[6] : kSinCosTab[12], K4 = odd ? kSinCosTab[7] : kSinCosTab[13],
+               K5 = odd ? kSinCosTab[8] : kSinCosTab[14], K6 = odd ? kSinCosTab[9] : kSinCosTab[15];
+#else
+  constexpr double INV_PIO2 = 0.6366197723675814, PIO2_1 = 1.5707963267341256,
+                   PIO2_1T = 6.077100506506192e-11, PIO2_1TT = 3.5215598651832e-27;
+  const double fn = std::nearbyint(x * INV_PIO2);
+  const int q = (int)fn & 3;
+  const bool odd = q & 1;
+  const double K1 = odd ? -1.66666666666666324348e-01 : 4.16666666666666019037e-02,
+               K2 = odd ? 8.33333333332248946124e-03 : -1.38888888888741095749e-03,
+               K3 = odd ? -1.98412698298579493134e-04 : 2.48015872894767294178e-05,
+               K4 = odd ? 2.75573137070700676789e-06 : -2.75573143513906633035e-07,
+               K5 = odd ? -2.50507602534068634195e-08 : 2.08757232129817482790e-09,
+               K6 = odd ? 1.58969099521155010221e-10 : -1.13596475577881948265e-11;
+#endif
+  const double r0 = x - fn * PIO2_1;
+  const double p = fn * PIO2_1T;
+  const double pe = fma(fn, PIO2_1T, -p);
+  const double rh = r0 - p;
+  const double bb = rh - r0;
+  const double rl = ((r0 - (rh - bb)) + (-p - bb)) - pe - fn * PIO2_1TT;
+  const double z = rh * rh;
+  const double zl = fma(rh, rh, -z) + 2.0 * rh * rl;
+  const double w = z * z;
+  // q odd: the sin kernel (head rh, m = c3 = z rh, ml = fma(z, rh, -c3) +
+  // zl rh); q even: the cos kernel (head a = 1 - z/2, m = w = z z, ml =
+  // fma(z, z, -w) + (2 z) zl) -- selects, no branch
+  const double hz = 0.5 * z, a = 1.0 - hz, al = (1.0 - a) - hz;
+  const double u = odd ? rh : z, vv = odd ? rh : 2.0 * z;
+  const double head = odd ? rh : a;
+  const double m = z * u;
+  const double ml = fma(z, u, -m) + zl * vv;
+  const double e = odd ? rl * fma(-0.5, z, 1.0) : al - 0.5 * zl;
+  const double t = m * K1, tl = fma(m, K1, -t) + ml * K1;
+  const double hh = head + t, ll = t - (hh - head);
+  const double tail = m * z * fma(z * w, fma(z, K6, K5), fma(z, fma(z, K4, K3), K2));
+  // sin: (t1l + s5) + rl (1 - z/2);  cos: ((al - zl/2) + t2l) + c6
+  const double a1 = odd ? tl : e, a2 = odd ? tail : tl, a3 = odd ? e : tail;
+  double r = hh + (ll + ((a1 + a2) + a3));
+  r = (q == 1 || q == 2) ? -r : r;
+  const double ax = x < 0 ? -x : x;
+  return ax < 1.4901161193847656e-08 ? 1.0 : r;  // tiny: cos x = 1
+}
+
 __host__ __device__ __forceinline__ bool trig_in_range(double x) {
   return x <= kTrigMax && x >= -kTrigMax;  // false for NaN too
 }

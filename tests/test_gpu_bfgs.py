@@ -156,7 +156,8 @@ def test_sqrt_free_convergence_and_guard_decisions(tmp_path):
     """The iteration tests decided without square roots (|g|^2 <= gsq_max,
     the squared curvature guard with its exact near-tie fallback) take the
     reference's decisions for every input: millions of random, boundary,
-    ulp-neighbour, zero, inf and NaN cases on the device."""
+    ulp-neighbour, zero, inf and NaN cases on the device.  Same tool: the
+    one-polynomial cos_fast equals sincos_fast's cosine bit for bit."""
     import os
     import subprocess
 

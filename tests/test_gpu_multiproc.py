@@ -142,3 +142,29 @@ def test_two_process_early_stop_semantics(z):
     # both shards were stopped by the one shared flag (each half has stopped runs)
     half = (cfg.N + 1) // 2
     assert np.any(s[:half] == 2) and np.any(s[half:] == 2)
+
+
+@pytest.mark.parametrize("exchange", ["collective", "peer"])
+def test_bench_two_ranks_prints_one_line(exchange):
+    """bench.py's N > 1 path (the driver's scaling run) end to end: two ranks
+    under torch.distributed.run on the one GPU (gloo; collective barrier or
+    the IPC peer exchange): every collective is taken by both ranks, rank 0
+    alone prints one JSON line with n_gpus = 2 and the whole-job count."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ZEUS_BENCH_DEVICE="0", ZEUS_BENCH_BACKEND="gloo",
+               ZEUS_PSO_EXCHANGE=exchange)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+           "--gpus", "2", "--config", "c1", "--steps", "2", "--warmup", "3",
+           "--no-cpu-baseline", "--no-north-star"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "start-sharded x2"
+    assert d["value"] > 0 and d["e2e"]["value"] > 0

@@ -343,7 +343,7 @@ def main():
     }
     if ns is not None:
         line["north_star"] = ns
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N = 1 figure
         c, secs, threads = cpu_reference_run(args.config, world, 42)
         line["cpu_baseline"] = {"value": c / secs, "unit": "starts/s", "cores": threads,
                                 "kind": "port",

@@ -152,11 +152,13 @@ def run_reference_arm(args, rank, world):
     from oracle import oracle as O
 
     O.build()
+    # each step times a bounded sample: the one-GPU share of the workload
+    # (the CPU rate is size-independent; N x the work would take minutes)
     for s in range(args.warmup):
-        cpu_reference_run(args.config, world, 42 + s)
+        cpu_reference_run(args.config, 1, 42 + s)
     conv = secs = 0.0
     for s in range(args.steps):
-        c, t, threads = cpu_reference_run(args.config, world, 42 + s)
+        c, t, threads = cpu_reference_run(args.config, 1, 42 + s)
         conv += c
         secs += t
     value = conv / secs
@@ -167,8 +169,9 @@ def run_reference_arm(args, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (Philox starts)",
         "config": {"workload": workload_name(args.config, world), "seed": "42+step"},
         "cpu_baseline": {"value": value, "unit": "starts/s", "cores": threads, "kind": "port",
-                         "sample": "full workload, deterministic (required_c=N); PSO on one "
-                                   "thread as in the reference, BFGS on a pthread pool"},
+                         "sample": workload_name(args.config, 1) + " per step (the one-GPU "
+                                   "share of the workload), deterministic (required_c=N); PSO "
+                                   "on one thread as in the reference, BFGS on a pthread pool"},
         "e2e": {"value": value, "unit": "starts/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

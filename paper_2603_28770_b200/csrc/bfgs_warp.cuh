@@ -52,9 +52,12 @@ struct BfgsWarp {
 #endif
 
   // Evaluate a batch: NH == 0 -> eval_batch over the warp; NH > 0 -> publish
-  // the task, all 32 (1+NH) threads run the term pass, warp 0 folds.
+  // the task, the NH helper warps run the term pass while warp 0 finishes the
+  // previous iteration's g.p reduction (ddir_io != null: its shuffle chain
+  // then overlaps the batch instead of delaying the task), warp 0 folds.
   __device__ __forceinline__ double evalb(const BfgsArgs& A, int B, const double* alphas, int d,
-                                          double* TT, int lane, double acc[Obj::NACC]) {
+                                          double* TT, int lane, double acc[Obj::NACC],
+                                          double* ddir_io = nullptr, double pd_part = 0.0) {
     if constexpr (NH == 0) {
       return eval_batch<Obj>(B, alphas, d, x, p, T, TT, A.tstride, A.bmax, lane, acc);
     } else {
@@ -66,21 +69,12 @@ struct BfgsWarp {
       PHASE(6);  // batch setup (alpha table, task)
       bar1(NT);  // A: task, x, p, alphas visible to the helpers
       PHASE(7);  // barrier A
-      const int nt = Obj::nterms(d);
-      const int total = (B > 0 ? B : 1) * nt;
-      bool oor = false;
-      if (total > 0)
-        term_pass<Obj, FastMath, NT>(B, nt, total, alphas, d, x, p, T, TT, A.tstride, A.bmax,
-                                     lane, oor, &tix);
-      PHASE(8);  // warp 0's share of the term pass
-      const bool any_oor = bar1_or(NT, oor);
+      if (ddir_io) *ddir_io = warp_sum_n<(DR > 0 && DR <= 16) ? 16 : 32>(pd_part);
+      PHASE(8);  // warp 0's g.p reduction (the helpers evaluate the terms)
+      const bool any_oor = bar1_or(NT, false);
       PHASE(9);  // barrier B (waits for the helpers' terms)
-      if (any_oor) {  // B: every term written
-        if (total > 0)
-          term_pass<Obj, PreciseMath, NT>(B, nt, total, alphas, d, x, p, T, TT, A.tstride,
-                                          A.bmax, lane, oor, &tix);
-        bar1(NT);
-      }
+      if (any_oor) bar1(NT);  // the helpers re-evaluate with libm
+      const int nt = Obj::nterms(d);
       const int nb = B > 0 ? B : 1;
       double f = 0.0;
       if (lane < nb) {
@@ -172,8 +166,8 @@ struct BfgsWarp {
     double f0 = 0.0;
     int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0, prev_trials = 1;
     double gsq = __longlong_as_double(0x7ff0000000000000LL);  // |g|^2 (|g| = inf: no gradient)
-    double ddir = 0.0;
-    bool pending = false;
+    double ddir = 0.0, pd_part = 0.0;
+    bool pending = false, ddir_pending = false;
 
     for (int i = d + lane; i < DR; i += 32)  // zero padding rows of row4
       row4[4 * i] = row4[4 * i + 1] = row4[4 * i + 2] = row4[4 * i + 3] = 0.0;
@@ -276,10 +270,16 @@ struct BfgsWarp {
             __syncwarp();
           }
           double accb[Obj::NACC];
-          // Armijo threshold of this lane's trial, formed before the batch
-          // so its latency hides behind the term pass (same ops, same order)
-          const double thr = f0 + A.c1 * atab[lane] * ddir;
-          const double fb = evalb(A, B, atab, d, TT, lane, accb);
+          // Armijo threshold of this lane's trial (same ops, same order):
+          // formed before the batch in warp mode (its latency hides behind
+          // the term pass); after it in helper mode, where g.p itself is
+          // reduced during the batch
+          double thr = 0.0;
+          if constexpr (NH == 0) thr = f0 + A.c1 * atab[lane] * ddir;
+          const double fb = evalb(A, B, atab, d, TT, lane, accb,
+                                  ddir_pending ? &ddir : nullptr, pd_part);
+          ddir_pending = false;
+          if constexpr (NH > 0) thr = f0 + A.c1 * atab[lane] * ddir;
           bool pass = false;
           if (lane < B) pass = fb <= thr;  // NaN fails
           const unsigned m = __ballot_sync(kFull, pass);
@@ -471,7 +471,14 @@ struct BfgsWarp {
 #pragma unroll
       for (int a = 0; a < Obj::NACC; ++a) acc[a] = acc_new[a];
       gsq = part[0];
-      ddir = warp_sum_n<(DR > 0 && DR <= 16) ? 16 : 32>(pd);  // np.dot(g, p) of the next line search
+      // np.dot(g, p) of the next line search: in helper mode the reduction
+      // runs during the next batch (evalb), here only the lane partial
+      if constexpr (NH > 0) {
+        pd_part = pd;
+        ddir_pending = true;
+      } else {
+        ddir = warp_sum_n<(DR > 0 && DR <= 16) ? 16 : 32>(pd);
+      }
       PHASE(4);  // ddir reduction + swap
       ++k;
       __syncwarp();
@@ -548,8 +555,9 @@ __global__ void __launch_bounds__(NH > 0 ? 32 * (NH + 1) : kBfgsWarps * 32,
   W.T = v;
   W.xbuf[0] = W.x;
   W.xbuf[1] = W.xn;
-  if constexpr (NH > 0) W.tix = term_idx<32 * (NH + 1)>(Obj::nterms(d) > 0 ? Obj::nterms(d) : 1,
-                                                      (int)threadIdx.x);
+  if constexpr (NH > 0)  // the helper warps alone cover a batch (warp 0 reduces g.p meanwhile)
+    W.tix = term_idx<32 * NH>(Obj::nterms(d) > 0 ? Obj::nterms(d) : 1,
+                              (int)threadIdx.x - 32);
   W.task = reinterpret_cast<HelperTask*>(sm + A.nalpha + A.warp_doubles);
 
   if constexpr (NH == 0) {
@@ -598,12 +606,12 @@ __global__ void __launch_bounds__(NH > 0 ? 32 * (NH + 1) : kBfgsWarps * 32,
       const int total = (B > 0 ? B : 1) * nt;
       bool oor = false;
       if (total > 0)
-        term_pass<Obj, FastMath, 32 * (NH + 1)>(B, nt, total, atab, d, x, W.p, W.T, TT,
-                                               A.tstride, A.bmax, tid, oor, &W.tix);
+        term_pass<Obj, FastMath, 32 * NH>(B, nt, total, atab, d, x, W.p, W.T, TT, A.tstride,
+                                          A.bmax, tid - 32, oor, &W.tix);
       if (bar1_or(32 * (NH + 1), oor)) {  // B
         if (total > 0)
-          term_pass<Obj, PreciseMath, 32 * (NH + 1)>(B, nt, total, atab, d, x, W.p, W.T, TT,
-                                                    A.tstride, A.bmax, tid, oor, &W.tix);
+          term_pass<Obj, PreciseMath, 32 * NH>(B, nt, total, atab, d, x, W.p, W.T, TT,
+                                               A.tstride, A.bmax, tid - 32, oor, &W.tix);
         bar1(32 * (NH + 1));
       }
     }

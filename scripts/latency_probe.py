@@ -40,7 +40,7 @@ k = int(out.iterations[0].item())
 if timing:
     L.zeus_debug_phase_cycles(buf, 0)
     names = ["line search (rest)", "gradient", "H pass", "8-value reduction+p'", "ddir+swap",
-             "prologue", "LS setup", "bar A", "term pass (warp 0)", "bar B", "folds"]
+             "prologue", "LS setup", "bar A", "g.p reduction (warp 0)", "bar B (helpers' term pass)", "folds"]
     print("warp phase cycles per iteration:", {n: round(buf[i] / max(k, 1)) for i, n in enumerate(names)})
     L.zeus_debug_team_phase_cycles(buf, 0)
     tn = ["line search", "gradient", "H pass", "8-value reduction+p'", "ddir"]

@@ -52,43 +52,51 @@ struct BfgsWarp {
 #endif
 
   // Evaluate a batch: NH == 0 -> eval_batch over the warp; NH > 0 -> publish
-  // the task, the NH helper warps run the term pass while warp 0 finishes the
-  // previous iteration's g.p reduction (ddir_io != null: its shuffle chain
-  // then overlaps the batch instead of delaying the task), warp 0 folds.
+  // the task (batch_publish), the NH helper warps run the term pass while
+  // warp 0 does work that needs no trial result (the run loop: the previous
+  // iteration's g.p reduction and the pending rank-2 update of H), then warp
+  // 0 waits for the terms and folds (batch_finish).
+  __device__ __forceinline__ void batch_publish(int B) {
+    const int lane = threadIdx.x & 31;  // (warp 0: == threadIdx.x)
+    (void)lane;
+    if (lane == 0) {
+      task->B = B;
+      task->xsel = (x == xbuf[0]) ? 0 : 1;
+    }
+    __syncwarp();
+    PHASE(6);  // batch setup (alpha table, task)
+    bar1(NT);  // A: task, x, p, alphas visible to the helpers
+    PHASE(7);  // barrier A
+  }
+  __device__ __forceinline__ double batch_finish(const BfgsArgs& A, int B, int d, int lane,
+                                                 double acc[Obj::NACC]) {
+    PHASE(8);  // warp 0's own work during the batch
+    const bool any_oor = bar1_or(NT, false);
+    PHASE(9);  // barrier B (waits for the helpers' terms)
+    if (any_oor) bar1(NT);  // the helpers re-evaluate with libm
+    const int nt = Obj::nterms(d);
+    const int nb = B > 0 ? B : 1;
+    double f = 0.0;
+    if (lane < nb) {
+#pragma unroll
+      for (int a = 0; a < Obj::NACC; ++a) {
+        const double* row = T + (a * A.bmax + lane) * A.tstride;
+        acc[a] = seq_fold<DR>(row, nt, Obj::init(a, d));
+      }
+      bool err = false;
+      f = Obj::finish(acc, d, err);
+    }
+    __syncwarp();
+    PHASE(10);  // reference-order folds
+    return f;
+  }
   __device__ __forceinline__ double evalb(const BfgsArgs& A, int B, const double* alphas, int d,
-                                          double* TT, int lane, double acc[Obj::NACC],
-                                          double* ddir_io = nullptr, double pd_part = 0.0) {
+                                          double* TT, int lane, double acc[Obj::NACC]) {
     if constexpr (NH == 0) {
       return eval_batch<Obj>(B, alphas, d, x, p, T, TT, A.tstride, A.bmax, lane, acc);
     } else {
-      if (lane == 0) {
-        task->B = B;
-        task->xsel = (x == xbuf[0]) ? 0 : 1;
-      }
-      __syncwarp();
-      PHASE(6);  // batch setup (alpha table, task)
-      bar1(NT);  // A: task, x, p, alphas visible to the helpers
-      PHASE(7);  // barrier A
-      if (ddir_io) *ddir_io = warp_sum_n<(DR > 0 && DR <= 16) ? 16 : 32>(pd_part);
-      PHASE(8);  // warp 0's g.p reduction (the helpers evaluate the terms)
-      const bool any_oor = bar1_or(NT, false);
-      PHASE(9);  // barrier B (waits for the helpers' terms)
-      if (any_oor) bar1(NT);  // the helpers re-evaluate with libm
-      const int nt = Obj::nterms(d);
-      const int nb = B > 0 ? B : 1;
-      double f = 0.0;
-      if (lane < nb) {
-#pragma unroll
-        for (int a = 0; a < Obj::NACC; ++a) {
-          const double* row = T + (a * A.bmax + lane) * A.tstride;
-          acc[a] = seq_fold<DR>(row, nt, Obj::init(a, d));
-        }
-        bool err = false;
-        f = Obj::finish(acc, d, err);
-      }
-      __syncwarp();
-      PHASE(10);  // reference-order folds
-      return f;
+      batch_publish(B);
+      return batch_finish(A, B, d, lane, acc);
     }
   }
 
@@ -274,12 +282,30 @@ struct BfgsWarp {
           // formed before the batch in warp mode (its latency hides behind
           // the term pass); after it in helper mode, where g.p itself is
           // reduced during the batch
-          double thr = 0.0;
-          if constexpr (NH == 0) thr = f0 + A.c1 * atab[lane] * ddir;
-          const double fb = evalb(A, B, atab, d, TT, lane, accb,
-                                  ddir_pending ? &ddir : nullptr, pd_part);
-          ddir_pending = false;
-          if constexpr (NH > 0) thr = f0 + A.c1 * atab[lane] * ddir;
+          double thr = 0.0, fb;
+          if constexpr (NH == 0) {
+            thr = f0 + A.c1 * atab[lane] * ddir;
+            fb = evalb(A, B, atab, d, TT, lane, accb);
+          } else {
+            batch_publish(B);
+            if (ddir_pending) {  // g.p of this line search, reduced during the batch
+              ddir = warp_sum_n<(DR > 0 && DR <= 16) ? 16 : 32>(pd_part);
+              ddir_pending = false;
+            }
+            if constexpr (DR > 0) {
+              if (pending) {  // the previous iteration's rank-2 update of H, also
+                const double aj = a_col[0], bj = b_col[0];  // during the batch
+#pragma unroll
+                for (int i = 0; i < DR; ++i) {
+                  const double2 r1 = *reinterpret_cast<const double2*>(row4 + 4 * i + 2);
+                  hreg[i] = fma(r1.x, aj, fma(r1.y, bj, hreg[i]));
+                }
+                pending = false;
+              }
+            }
+            fb = batch_finish(A, B, d, lane, accb);
+            thr = f0 + A.c1 * atab[lane] * ddir;
+          }
           bool pass = false;
           if (lane < B) pass = fb <= thr;  // NaN fails
           const unsigned m = __ballot_sync(kFull, pass);
@@ -356,9 +382,12 @@ struct BfgsWarp {
         for (int i = 0; i < DR; ++i) {
           const double2 r0 = *reinterpret_cast<const double2*>(row4 + 4 * i);
           const double2 r1 = *reinterpret_cast<const double2*>(row4 + 4 * i + 2);
-          const double upd = fma(r1.x, aj, fma(r1.y, bj, hreg[i]));
-          const double h = pending ? upd : hreg[i];
-          hreg[i] = h;
+          double h = hreg[i];
+          if constexpr (NH == 0) {  // (helper mode applied it during the batch)
+            const double upd = fma(r1.x, aj, fma(r1.y, bj, h));
+            h = pending ? upd : h;
+            hreg[i] = h;
+          }
           uq[i & 3] = fma(h, r0.x, uq[i & 3]);
           wq[i & 3] = fma(h, r0.y, wq[i & 3]);
         }

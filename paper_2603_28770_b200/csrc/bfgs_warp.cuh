@@ -303,8 +303,8 @@ struct BfgsWarp {
                 pending = false;
               }
             }
+            thr = f0 + A.c1 * atab[lane] * ddir;  // also inside the batch window
             fb = batch_finish(A, B, d, lane, accb);
-            thr = f0 + A.c1 * atab[lane] * ddir;
           }
           bool pass = false;
           if (lane < B) pass = fb <= thr;  // NaN fails

@@ -455,11 +455,13 @@ struct BfgsWarp {
         warp_sum8<(DR > 0 && DR <= 16) ? 16 : 32>(part);
       }
       const double curv = part[1];
-      pending = curvature_update(curv, part[2], part[3]);  // bfgs.py:69-71
+      // 1/curv issued next to the guard (straight-line), so the two overlap
+      const double rinv = 1.0 / curv;
+      pending = curvature_update_sl(curv, part[2], part[3]);  // bfgs.py:69-71
       double pd = 0.0;
       __syncwarp();  // row4 (dx/u of the previous iteration) fully consumed
       {
-        const double rho = pending ? 1.0 / curv : 0.0;
+        const double rho = pending ? rinv : 0.0;
         const double cc = pending ? fma(rho * rho, part[4], rho) : 0.0;
         const double ug = part[5], xg = part[6];
         for (int c = 0; c < C; ++c) {

@@ -12,6 +12,7 @@ __global__ void k(const double* c, const double* a, const double* b, int n, int*
   if (i >= n) return;
   bool ref = !(c[i] <= kCurvatureFloor * sqrt(a[i]) * sqrt(b[i]));
   if (ref != curvature_update(c[i], a[i], b[i])) atomicAdd(bad, 1);
+  if (ref != curvature_update_sl(c[i], a[i], b[i])) atomicAdd(bad, 1);
 }
 // cos_fast(x) == sincos_fast(x).c bit for bit
 __global__ void kc(const double* x, int n, int* bad) {

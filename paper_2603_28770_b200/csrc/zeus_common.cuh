@@ -47,6 +47,22 @@ __device__ __forceinline__ bool curvature_update(double curv, double dxdx, doubl
   }
   return !(curv <= kCurvatureFloor * sqrt(dxdx) * sqrt(dgdg));
 }
+// The same decision with the common case in straight-line code (selects), so
+// its arithmetic can interleave with an independent computation issued next
+// to it (the 1/curvature division of the BFGS update); only a near tie or an
+// out-of-range operand takes the branch to the reference expression.
+__device__ __forceinline__ bool curvature_update_sl(double curv, double dxdx, double dgdg) {
+  constexpr double kMin = 2.2250738585072014e-308, kMax = 1e300;
+  const double q = curv * curv;
+  const double t = (kCurvatureFloor * kCurvatureFloor) * dxdx;
+  const double r = t * dgdg;
+  const bool normal = t >= kMin && t <= kMax && r >= kMin && r <= kMax && q >= kMin && q <= kMax;
+  const bool nonpos = curv <= 0.0 && dxdx <= 1e300 && dgdg <= 1e300;
+  const bool up = normal && q > r * (1.0 + 1e-9);
+  const bool dn = normal && q < r * (1.0 - 1e-9);
+  if (nonpos || up || dn) return up && !nonpos;
+  return !(curv <= kCurvatureFloor * sqrt(dxdx) * sqrt(dgdg));
+}
 constexpr unsigned kFull = 0xffffffffu;
 
 // ---------------------------------------------------------------------------

@@ -242,3 +242,24 @@ def test_devices_single_process_early_stop(z):
     s = r.per_run.status_codes
     assert len(s) == 20000 and r.converged_count >= 100
     assert np.any(s[:10000] == 2) and np.any(s[10000:] == 2)   # both shards stopped
+
+
+def test_devices_with_a_user_objective(z):
+    """devices= with a device plug-in (shards repeated on the one GPU): the
+    NVRTC module's fused PSO with the peer exchange and its BFGS kernels give
+    the one-GPU results bit for bit."""
+    src = """
+template <class T, class X>
+__device__ T objective(const X& x, int d, const double* data, bool& err) {
+  T s = 0.0;
+  for (int i = 0; i < d; ++i) s = s + data[i] * x(i) * x(i) - zu::cos(3.0 * x(i));
+  return s;
+}"""
+    f = z.DeviceObjective(src, dim=5, data=[1.0, 2.0, 0.5, 1.5, 1.0], name="wavy5")
+    cfg = z.ZeusConfig(N=3000, dim=5, range=(-2.0, 2.0), iter_pso=4, iter_bfgs=500, seed=6,
+                       deterministic=True)
+    one = z.zeus_run(f, cfg)
+    two = z.zeus_run(f, cfg, devices=[0, 0])
+    assert np.array_equal(one.per_run.x_final, two.per_run.x_final)
+    assert np.array_equal(one.per_run.status_codes, two.per_run.status_codes)
+    assert one.best == two.best and one.pso_best_before_bfgs == two.pso_best_before_bfgs

@@ -209,10 +209,11 @@ def reduce_best(f_final, status) -> int:
 
 def zeus_run(obj, d: int, n: int, seed: int, lower: float, upper: float, iter_pso: int,
              iter_bfgs: int, theta=1e-6, threads=None, w=0.5, c1_pso=1.2, c2_pso=1.5,
-             c1_ls=0.3, alpha0=1.0, iter_ls=20, shrink=0.5):
+             c1_ls=0.3, alpha0=1.0, iter_ls=20, shrink=0.5, return_swarm=False):
     """Deterministic zeus_run (driver.py:220-265, required_c = N): PSO on one
     thread (as the reference), BFGS on a pthread pool.  Returns
-    (converged_count, best_index, pso_best, BfgsResult)."""
+    (converged_count, best_index, pso_best, BfgsResult) (+ the final Swarm
+    when ``return_swarm``)."""
     if threads is None:
         threads = os.cpu_count() or 1
     x = np.empty((n, d)); v = np.empty((n, d)); p = np.empty((n, d)); pv = np.empty(n)
@@ -228,4 +229,7 @@ def zeus_run(obj, d: int, n: int, seed: int, lower: float, upper: float, iter_ps
     res = BfgsResult(xf, arr["f_final"].copy(), arr["grad_norm"].copy(),
                      arr["iterations"].copy(), arr["status"].copy(),
                      arr["ls_trials"].copy(), arr["grad_evals"].copy())
-    return int(np.sum(res.status == 0)), int(best), pb.value, res
+    ret = (int(np.sum(res.status == 0)), int(best), pb.value, res)
+    if return_swarm:
+        ret += (Swarm(x, v, p, pv, gX, pb.value),)
+    return ret

@@ -406,26 +406,40 @@ int oracle_hessian_update(int d, double *H, const double *dx, const double *dg) 
   double rho = 1.0 / curvature;
   size_t dd = (size_t)d * (size_t)d;
   double *V = (double *)malloc(sizeof(double) * dd);
+  double *VT = (double *)malloc(sizeof(double) * dd);
   double *T = (double *)malloc(sizeof(double) * dd);
   double *U = (double *)malloc(sizeof(double) * dd);
   for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j)
+    for (int j = 0; j < d; ++j) {
       V[i * d + j] = (i == j ? 1.0 : 0.0) - rho * (dx[i] * dg[j]);
-  for (int i = 0; i < d; ++i) /* T = V @ H */
-    for (int j = 0; j < d; ++j) {
-      double s = 0.0;
-      for (int k = 0; k < d; ++k) s += V[i * d + k] * H[k * d + j];
-      T[i * d + j] = s;
+      VT[j * d + i] = V[i * d + j];
     }
-  for (int i = 0; i < d; ++i) /* U = T @ V^T + rho dx dx^T */
-    for (int j = 0; j < d; ++j) {
-      double s = 0.0;
-      for (int k = 0; k < d; ++k) s += T[i * d + k] * V[j * d + k];
-      U[i * d + j] = s + rho * (dx[i] * dx[j]);
+  /* T = V @ H and U = T @ V^T.  Each element is the k-ordered sum
+   * ((0 + a_0 b_0) + a_1 b_1) + ... exactly as a dot-product loop would form
+   * it; the loops run i-k-j so the j loop is a plain (vectorisable) axpy that
+   * does not reorder any element's additions. */
+  for (size_t e = 0; e < dd; ++e) T[e] = 0.0;
+  for (int i = 0; i < d; ++i)
+    for (int k = 0; k < d; ++k) {
+      double a = V[i * d + k];
+      const double *Hk = H + (size_t)k * d;
+      double *Ti = T + (size_t)i * d;
+      for (int j = 0; j < d; ++j) Ti[j] += a * Hk[j];
     }
+  for (size_t e = 0; e < dd; ++e) U[e] = 0.0;
+  for (int i = 0; i < d; ++i)
+    for (int k = 0; k < d; ++k) {
+      double a = T[i * d + k];
+      const double *Vk = VT + (size_t)k * d;
+      double *Ui = U + (size_t)i * d;
+      for (int j = 0; j < d; ++j) Ui[j] += a * Vk[j];
+    }
+  for (int i = 0; i < d; ++i) /* + rho dx dx^T */
+    for (int j = 0; j < d; ++j) U[i * d + j] = U[i * d + j] + rho * (dx[i] * dx[j]);
   for (int i = 0; i < d; ++i)
     for (int j = 0; j < d; ++j) H[i * d + j] = 0.5 * (U[i * d + j] + U[j * d + i]);
   free(V);
+  free(VT);
   free(T);
   free(U);
   return 1;

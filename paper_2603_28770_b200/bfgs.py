@@ -113,6 +113,10 @@ def bfgs_run(
     x = np.asarray(x0, dtype=np.float64).ravel()
     obj = objective_id(f, x.shape[0])
     dev = _device.require_device()
+    if not isinstance(obj, int):
+        from .driver import check_objective_device
+
+        check_objective_device(obj, dev)
     full = _single(obj, x, theta, iter_bfgs, ls, dev)
     if stop_probe is None:
         return full

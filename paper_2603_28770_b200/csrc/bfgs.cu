@@ -136,9 +136,6 @@ extern "C" {
 
 #ifdef ZEUS_PHASE_TIMING
 // diagnostics only (not in include/zeus_b200.h): copy out / reset the phase cycles
-int zeus_debug_team_phase_cycles(unsigned long long* out, int reset) {
-  return zeus::team_phase_cycles(out, reset);
-}
 int zeus_debug_phase_cycles(unsigned long long* out, int reset) {
   if (cudaMemcpyFromSymbol(out, zeus_phase_cycles, sizeof(unsigned long long) * 16) != cudaSuccess)
     return -2;
@@ -170,7 +167,7 @@ size_t zeus_bfgs_workspace_bytes(int d, int64_t n) {
   size_t extra = 0;
   if (promotes(d) || d <= 16) extra = 2 * (size_t)n * carry_stride_for(d) * sizeof(double);
   const BfgsPlan P = bfgs_plan(d, 2, d, 1024);
-  if (P.dr > 0 || P.smem_h || bfgs_team_covers(ZEUS_OBJ_RASTRIGIN, d)) return kWsHeader + extra;
+  if (P.dr > 0 || P.smem_h || bfgs_wide_covers(ZEUS_OBJ_RASTRIGIN, d)) return kWsHeader + extra;
   int sms = current_sm_count();
   if (sms < 1) sms = 148;
   return kWsHeader + (size_t)global_h_blocks(sms) * kBfgsWarps * (size_t)d * d * sizeof(double);
@@ -212,8 +209,6 @@ int zeus_bfgs(int obj, int d, int64_t n, const double* x0, int64_t ldx,
   if (rc) return rc;
   if (bfgs_wide_covers(obj, d) && !getenv_flag("ZEUS_NO_WIDE")) {
     rc = launch_bfgs_wide(obj, A, s);
-  } else if (bfgs_team_covers(obj, d) && !getenv_flag("ZEUS_NO_TEAM")) {
-    rc = launch_bfgs_team(obj, A, s);
   } else {
     const int stride = carry_stride_for(d);
     double* c1 = (double*)((char*)workspace + kWsHeader);

@@ -1,6 +1,7 @@
-// bfgs_common.cuh -- pieces shared by the warp-per-start (bfgs.cu) and the
-// CTA-per-start (bfgs_team.cu) BFGS kernels: launch arguments, the trial-point
-// accessor, the speculative term pass, gradient helpers.
+// bfgs_common.cuh -- pieces shared by the BFGS kernel families (thread, warp
+// and CTA-helper tiers in bfgs.cu / bfgs_thread.cu, the wide kernels in
+// bfgs_wide.cu): launch arguments, the trial-point accessor, the speculative
+// term pass, gradient helpers.
 #pragma once
 #ifndef __CUDACC_RTC__
 #include <algorithm>
@@ -38,7 +39,7 @@ struct BfgsArgs {
   int bmax;          // max trials per speculative batch
   int nalpha;        // alpha table length (block smem)
   // straggler promotion (small d): a start still running at iteration k1 is
-  // handed from the warp kernel to the CTA-team kernel through a carry record
+  // handed from one tier to the next through a carry record
   int k1;                          // 0: never promote
   double* carry;                   // [capacity][carry_stride] state records
   int carry_stride;                // doubles per record
@@ -286,12 +287,6 @@ __device__ __forceinline__ bool grad_needs_slow(const double* xs, int d, int lan
 
 
 #ifndef __CUDACC_RTC__
-// Launch of the CTA-per-start kernel family (bfgs_team.cu).  Returns
-// ZEUS_ERR_UNSUPPORTED when no team shape covers (obj, d).
-int launch_bfgs_team(int obj, BfgsArgs A, cudaStream_t s);
-bool bfgs_team_covers(int obj, int d);
-int team_phase_cycles(unsigned long long* out, int reset);  // -DZEUS_PHASE_TIMING only
-
 // Launch of the thread-per-start kernel for d <= 16 (bfgs_thread.cu).
 int launch_bfgs_thread(int obj, BfgsArgs A, cudaStream_t s);
 bool bfgs_thread_covers(int obj, int d);

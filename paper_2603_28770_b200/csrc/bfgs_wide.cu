@@ -2,8 +2,8 @@
 // two WARPS per start, built for throughput (the 1M-start 50-D targets and
 // config 4's 100-D Rosenbrock).
 //
-// Why a second kernel family next to the CTA-per-start team kernel
-// (bfgs_team.cu): at d = 50 a team start costs ~7,300 cycles of wall time per
+// Why not one CTA per start (the round-1 design, measured and retired): at
+// d = 50 such a start costs ~7,300 cycles of wall time per
 // iteration, 55% of it in the CTA-synchronised line search and 24% in CTA
 // reductions, and only 4 starts fit an SM (scripts/phase_probe.py).  Here a
 // start's state is spread over the lanes of W = 1 warp (d <= 64) or W = 2
@@ -36,7 +36,7 @@
 //     dx.g', w.g' -> curvature guard (bfgs.py:69-71), rho, the next direction
 //     p' = -H' g' = -(w - rho dx (u.g') - rho u (dx.g') + c dx (dx.g'));
 //  5. g'.p' (the next line search's ddir) by one butterfly.
-// Objective folds for d > 16 are trees (as in the team kernel): f agrees with
+// Objective folds for d > 16 are trees: f agrees with
 // the reference's sequential fold to ~1 ulp, inside the stated tolerance.
 #include "bfgs_common.cuh"
 

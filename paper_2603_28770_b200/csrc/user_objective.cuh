@@ -93,8 +93,11 @@ __device__ __forceinline__ auto div(A a, B b, bool& err) -> decltype(a / b) {
 }
 // powf(base, exponent) (autodiff.py:230-240, Dual.__pow__ 133-161)
 __device__ __forceinline__ double pow(double b, double e, bool& err) {
+  // math.pow raises ValueError (-> DomainError, autodiff.py:46-58) for a
+  // fractional power of a negative base and for a zero base with a negative
+  // exponent; overflow follows IEEE to +-inf like _safe_pow
   const double r = ::pow(b, e);
-  if (b < 0.0 && e != ::floor(e)) err = true;  // fractional power of a negative
+  if ((b < 0.0 && e != ::floor(e)) || (b == 0.0 && e < 0.0)) err = true;
   return r;
 }
 __device__ __forceinline__ Dual pow(Dual b, double e, bool& err) {

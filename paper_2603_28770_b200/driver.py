@@ -221,6 +221,38 @@ def _peer_exchange(process_group, world: int) -> bool:
     return not engine._host_backend(process_group)
 
 
+def _broadcast_best(per_run, bidx: int, owner: int, d: int, group, dev) -> BfgsOutcome:
+    """The best outcome from the rank whose table holds it (group rank
+    ``owner`` always does: it ran that start) to every rank."""
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    row = torch.zeros(d + 4, dtype=torch.float64)
+    if rank == owner:
+        o = per_run[bidx]
+        row[:d] = torch.tensor(o.x_final, dtype=torch.float64)
+        row[d:] = torch.tensor([o.f_final, o.grad_norm, o.iterations, STATUSES.index(o.status)],
+                               dtype=torch.float64)
+    src = dist.get_global_rank(group, owner) if group is not None else owner
+    if not engine._host_backend(group):
+        row = row.to(dev)
+    dist.broadcast(row, src=src, group=group)
+    r = row.cpu().numpy()
+    return BfgsOutcome(x_final=tuple(float(v) for v in r[:d]), f_final=float(r[d]),
+                       grad_norm=float(r[d + 1]), iterations=int(r[d + 2]),
+                       status=STATUSES[int(r[d + 3])])
+
+
+def _gather_mode(gather) -> str:
+    if gather is True or gather == "all":
+        return "all"
+    if gather is False or gather == "local":
+        return "local"
+    if gather == "root":
+        return "root"
+    raise ValueError("gather must be 'root', 'all' (True) or False")
+
+
 def _dist_world(process_group):
     if not torch.distributed.is_available() or not torch.distributed.is_initialized():
         return 0, 1
@@ -383,9 +415,17 @@ def _zeus_run_devices(obj, cfg: ZeusConfig, devs, starts, within, t0) -> ZeusRes
                       device_time=span(0, 3), stats=stats)
 
 
+def check_objective_device(obj, dev) -> None:
+    """A DeviceObjective's NVRTC module and data live on the device it was
+    built for; launching it on another device would cross contexts."""
+    if obj.device.index != torch.device(dev).index:
+        raise ValueError(f"DeviceObjective {obj.name!r} was compiled for cuda:{obj.device.index}, "
+                         f"not cuda:{torch.device(dev).index}: build it with device=")
+
+
 def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
              process_group=None, starts: Optional[np.ndarray] = None,
-             gather: bool = True, within=None, devices=None) -> ZeusResult:
+             gather="root", within=None, devices=None) -> ZeusResult:
     """Run the full pipeline on registered objective ``f`` (driver.py:220-265).
 
     Extensions (keyword-only, defaults reproduce the reference):
@@ -394,7 +434,11 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
                     the world group when torch.distributed is initialised).
       starts        host-supplied BFGS starts [N][dim]: skips PSO (used to
                     decouple BFGS parity from PSO libm flips).
-      gather        False keeps per_run local to this rank's shard.
+      gather        several ranks: "root" (default) gives group rank 0, the
+                    caller's process, per_run over all N starts and the
+                    other ranks their own shard; "all" (or True) gives every
+                    rank all N; False keeps per_run local to each shard.
+                    ``best`` is the global best on every rank.
       within        (optimum, radius): count the starts whose final point lies
                     within radius of optimum on device (bench.py:131-141),
                     reported as stats.n_within (summed over ranks).
@@ -414,6 +458,8 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
     """
     t0 = time.perf_counter()
     obj = objective_id(f, cfg.dim)
+    if within is not None and len(within[0]) != cfg.dim:
+        raise ValueError("within: optimum must have dim coordinates")
     if devices is not None:
         if isinstance(devices, int):
             devices = list(range(devices))
@@ -430,9 +476,13 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
                 raise NotImplementedError(
                     "a user objective is compiled for one device: run one process per GPU "
                     "(torchrun) to use several GPUs")
+            if not isinstance(obj, int):
+                check_objective_device(obj, devs[0])
             return _zeus_run_devices(obj, cfg, devs, starts, within, t0)
         device = devs[0]
     dev = _device.require_device(device)
+    if not isinstance(obj, int):
+        check_objective_device(obj, dev)
     rank, world = _dist_world(process_group)
     N, d = cfg.N, cfg.dim
     lo, hi = engine.shard_bounds(N, rank, world)
@@ -537,27 +587,38 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
     # ---- results to host (part of the end-to-end wall time): the per-start
     # columns are packed on the device into two row-major tables ([n][d + 2]
     # f64: x, f, |g|; [n][4] i32: k, status, trials, gradients) and copied
-    # with one pinned, asynchronous D2H each; the host arrays are views
+    # with one pinned, asynchronous D2H each; the host arrays are views.
+    # Several ranks: the packed shards (padded to ceil(N / world) rows) are
+    # gathered to group rank 0 (gather="root", the caller's copy) or to every
+    # rank (gather="all" / True); gather=False keeps the local shard.
+    mode = _gather_mode(gather)
+    if early and not device_stop and mode == "root":
+        mode = "all"  # the sequential prefix cut needs the whole table on every rank
     per = -(-N // world)
-    if world > 1 and gather:
-        xs = _gather_rows(out.x_final[:, :n], per, world, process_group)[:, :N]
-        cols = [_gather_rows(t[:n], per, world, process_group)[:N]
-                for t in (out.f_final, out.grad_norm, out.iterations, out.status,
-                          out.ls_trials, out.grad_evals)]
-        base = 0
-    else:
-        xs = out.x_final[:, :n]
-        cols = [t[:n] for t in (out.f_final, out.grad_norm, out.iterations, out.status,
-                                out.ls_trials, out.grad_evals)]
-        base = lo
-    m_rows = xs.shape[1]
-    fpack = torch.empty((m_rows, d + 2), dtype=torch.float64, device=dev)
-    fpack[:, :d] = xs.t()
-    fpack[:, d] = cols[0]
-    fpack[:, d + 1] = cols[1]
-    ipack = torch.empty((m_rows, 4), dtype=torch.int32, device=dev)
-    for c, t in enumerate((cols[2], cols[3], cols[4], cols[5])):
-        ipack[:, c] = t
+    fpack = torch.empty((per if world > 1 else n, d + 2), dtype=torch.float64, device=dev)
+    fpack[:n, :d] = out.x_final[:, :n].t()
+    fpack[:n, d] = out.f_final[:n]
+    fpack[:n, d + 1] = out.grad_norm[:n]
+    ipack = torch.zeros((fpack.shape[0], 4), dtype=torch.int32, device=dev)
+    for c, t in enumerate((out.iterations, out.status, out.ls_trials, out.grad_evals)):
+        ipack[:n, c] = t[:n]
+    base = lo
+    if world > 1 and mode == "local":
+        fpack, ipack = fpack[:n], ipack[:n]
+    elif world > 1:
+        if mode == "all":
+            gf = engine.all_gather_flat(fpack.view(-1), process_group)
+            gi = engine.all_gather_flat(ipack.view(-1), process_group)
+        else:
+            gf = engine.gather_root_flat(fpack.view(-1), process_group)
+            gi = engine.gather_root_flat(ipack.view(-1), process_group)
+        if gf is not None:  # this rank holds the whole table
+            fpack = gf.view(world * per, d + 2)[:N]
+            ipack = gi.view(world * per, 4)[:N]
+            base = 0
+        else:
+            fpack, ipack = fpack[:n], ipack[:n]
+    m_rows = fpack.shape[0]
     # scalars in one small table: tallies[4], the PSO best f, every rank's [f, idx]
     spack = torch.empty(5 + best_dev.numel(), dtype=torch.float64, device=dev)
     spack[0:4] = tallies
@@ -603,9 +664,9 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
         # sequential early stop reports a prefix: count inside it (host columns)
         tgt = np.asarray([float(v) for v in within[0]], dtype=np.float64)
         n_in = int(np.count_nonzero(np.linalg.norm(x_host[:m] - tgt, axis=1) < within[1]))
-    if not 0 <= bidx < m:
-        # best lives on another rank and per_run is local (gather=False)
-        best = None
+    if world > 1 and not (early and not device_stop):
+        # the global best on every rank: its owner broadcasts the row
+        best = _broadcast_best(per_run, bidx, gidx // per, d, process_group, dev)
     else:
         best = per_run[bidx]
     stats = RunStats(iterations=it_h[:m], ls_trials=ls_h[:m], grad_evals=ge_h[:m],

@@ -242,6 +242,26 @@ def all_gather_flat(t: torch.Tensor, group=None) -> torch.Tensor:
     return out
 
 
+def gather_root_flat(t: torch.Tensor, group=None):
+    """Gather equal-size 1-D shards to group rank 0 only: rank 0 gets
+    [world * len(t)] in rank order, the other ranks None (one collective,
+    no redundant copies of the whole table on every rank)."""
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dst = dist.get_global_rank(group, 0) if group is not None else 0
+    src = t.contiguous()
+    host = _host_backend(group) and src.is_cuda
+    if host:
+        src = src.cpu()
+    parts = [torch.empty_like(src) for _ in range(world)] if rank == 0 else None
+    dist.gather(src, parts, dst=dst, group=group)
+    if rank != 0:
+        return None
+    out = torch.cat(parts)
+    return out.to(t.device) if host else out
+
+
 def all_reduce_sum(t: torch.Tensor, group=None) -> None:
     """In-place sum over ranks (status tallies)."""
     import torch.distributed as dist
@@ -298,12 +318,25 @@ class StopBlock:
         src = dist.get_global_rank(group, 0) if group is not None else 0
         handle = ctypes.create_string_buffer(64)
         ptr = ctypes.c_void_p()
+        ok = True
         if rank == 0:
-            _capi.check(L.zeus_stop_block_create(ctypes.byref(ptr), handle), "stop block create")
-        box = [bytes(handle.raw) if rank == 0 else None]
+            ok = L.zeus_stop_block_create(ctypes.byref(ptr), handle) == 0
+        box = [bytes(handle.raw) if (rank == 0 and ok) else None]
         dist.broadcast_object_list(box, src=src, group=group)
         if rank != 0:
-            _capi.check(L.zeus_stop_block_open(box[0], ctypes.byref(ptr)), "stop block open")
+            ok = box[0] is not None and L.zeus_stop_block_open(box[0], ctypes.byref(ptr)) == 0
+        # agreed outcome: a rank that cannot map the block must not leave the
+        # others waiting in arm()'s barriers -- every rank raises together
+        votes = [None] * dist.get_world_size(group)
+        dist.all_gather_object(votes, bool(ok), group=group)
+        if not all(votes):
+            why = L.zeus_last_error().decode(errors="replace") if not ok else "a peer rank failed"
+            if ok and ptr.value:
+                L.zeus_stop_block_close(ptr.value, int(rank == 0))
+            raise RuntimeError(
+                "cross-GPU early stop (workers > 0, required_c < N) needs every rank to map "
+                f"rank 0's stop block over CUDA IPC / peer access ({why}); run with "
+                "workers=0 (sequential semantics, exact) or deterministic=True")
         blk = cls(int(ptr.value), rank == 0)
         cls._cache[key] = blk
         return blk

@@ -78,7 +78,7 @@ def xdiff(a, b):
 # two exact-arithmetic-equivalent trajectories may stop at different points of
 # that ball; f within 1e-10 max(1,|f|) (1e-6 for runs that hit the cap at a
 # gradient kink).
-X_TOL, X_TOL_CONVERGED = 1e-6, 1e-5
+X_TOL, X_TOL_CONVERGED = 1e-6, 1e-6
 
 
 def assert_outcomes_close(x, f, s, ref_x, ref_f, ref_s, label="", ref_gn=None):
@@ -105,3 +105,84 @@ def assert_outcomes_close(x, f, s, ref_x, ref_f, ref_s, label="", ref_gn=None):
     df = xdiff(np.asarray(f)[fin], np.asarray(ref_f)[fin])
     assert np.all(df <= ftol * np.maximum(1, np.abs(np.asarray(ref_f)[fin]))), label
     return dx
+
+
+def parity_report(label, x, f, gn, k, s, ref):
+    """Per-start comparison of a device result with the oracle's BfgsResult
+    on identical starts.  Prints (and returns) the numbers the north-star
+    parity bar is stated in: status flips, max |dx|_inf, max relative |df|,
+    the |dk| histogram and the bit-identical fraction.  Each flip is listed
+    with both gradient norms and iteration counts."""
+    s = np.asarray(s).astype(np.int64)
+    rs = np.asarray(ref.status).astype(np.int64)
+    flips = np.flatnonzero(s != rs)
+    same = s == rs
+    dx = np.max(xdiff(x, ref.x_final), axis=1)
+    rf = np.asarray(ref.f_final)
+    df = xdiff(f, rf) / np.maximum(1.0, np.abs(np.where(np.isfinite(rf), rf, 1.0)))
+    dk = np.abs(np.asarray(k, dtype=np.int64) - np.asarray(ref.iterations, dtype=np.int64))
+    hist = np.bincount(np.minimum(dk, 10), minlength=11)
+    bit = float(np.mean(np.all(np.asarray(x) == ref.x_final, axis=1)))
+    out = dict(n=len(s), flips=len(flips), max_dx=float(dx[same].max(initial=0.0)),
+               max_df=float(df[same].max(initial=0.0)), dk_mean=float(dk.mean()),
+               dk_max=int(dk.max(initial=0)), bit_identical_x=bit,
+               statuses={int(c): int(np.sum(rs == c)) for c in np.unique(rs)})
+    print(f"\n[parity] {label}: {out}")
+    print(f"[parity] {label}: |dk| histogram 0..9,>=10: {hist.tolist()}")
+    for i in flips[:20]:
+        print(f"[parity] {label}: flip start {i}: device status {s[i]} |g| {gn[i]:.3e} k {k[i]}"
+              f" / oracle status {rs[i]} |g| {ref.grad_norm[i]:.3e} k {ref.iterations[i]}")
+    return out
+
+
+FLOOR_GN = 1e-4   # a status flip must be a start stalled near theta on both sides
+
+
+class Sub:
+    """Per-start columns of a result at the given indices."""
+
+    def __init__(self, pr, idx=None):
+        sel = slice(None) if idx is None else idx
+        self.x_final = pr.x_final[sel]
+        self.f_final = pr.f_final[sel]
+        self.grad_norm = pr.grad_norm[sel]
+        self.iterations = pr.iterations[sel]
+        self.status_codes = np.asarray(pr.status_codes[sel]).astype(np.int64)
+
+
+def disagreements(a_s, a_x, a_gn, b_s, b_x, b_gn):
+    """(flips, different minima) between two outcome sets on the same starts."""
+    flips = np.flatnonzero(a_s != b_s)
+    same = a_s == b_s
+    dx = np.max(xdiff(a_x, b_x), axis=1)
+    basins = np.flatnonzero(same & (dx > 1e-6))
+    return flips, basins
+
+
+def gate(label, dev, ref, floor_count):
+    """The bar stated in the module docstring; returns the report."""
+    rep = parity_report(label, dev.x_final, dev.f_final, dev.grad_norm, dev.iterations,
+                        dev.status_codes, ref)
+    flips, basins = disagreements(dev.status_codes, dev.x_final, dev.grad_norm,
+                                  np.asarray(ref.status), ref.x_final, ref.grad_norm)
+    for i in basins[:10]:
+        print(f"[parity] {label}: different minimum at start {i}: f {dev.f_final[i]!r} vs "
+              f"{ref.f_final[i]!r}, |g| {dev.grad_norm[i]:.2e} / {ref.grad_norm[i]:.2e}, "
+              f"k {dev.iterations[i]} / {ref.iterations[i]}")
+    n_dis = len(flips) + len(basins)
+    allowed = 2 * floor_count + 2
+    print(f"[parity] {label}: {len(flips)} flips + {len(basins)} different minima = {n_dis} "
+          f"(noise floor {floor_count}, allowed {allowed})")
+    gmax = np.maximum(dev.grad_norm[flips], np.asarray(ref.grad_norm)[flips])
+    assert np.all(gmax < FLOOR_GN), (label, flips[gmax >= FLOOR_GN][:10])
+    assert n_dis <= allowed, (label, n_dis, allowed)
+    keep = np.ones(len(dev.status_codes), dtype=bool)
+    keep[flips] = False
+    keep[basins] = False
+    assert_outcomes_close(dev.x_final[keep], dev.f_final[keep], dev.status_codes[keep],
+                          ref.x_final[keep], ref.f_final[keep], np.asarray(ref.status)[keep],
+                          label, np.asarray(ref.grad_norm)[keep])
+    rep["disagreements"] = n_dis
+    return rep
+
+

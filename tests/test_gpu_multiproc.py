@@ -40,7 +40,7 @@ def _cfg(z, case):
                                      iter_bfgs=1000, required_c=100, workers=2, seed=5)
 
 
-def _worker(rank, world, port, q, case):
+def _worker(rank, world, port, q, case, gather="root"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch.distributed as dist
@@ -80,20 +80,22 @@ def _worker(rank, world, port, q, case):
             dist.barrier()
             return
         fn, cfg = _cfg(z, case)
-        r = z.zeus_run(fn, cfg)
+        r = z.zeus_run(fn, cfg, gather=gather)
         pr = r.per_run
+        lo, _ = engine.shard_bounds(cfg.N, rank, world)
         q.put((rank, pr.x_final.copy(), pr.f_final.copy(), pr.status_codes.copy(),
-               pr.iterations.copy(), pr.grad_norm.copy(), r.best.f_final, r.converged_count,
-               r.pso_best_before_bfgs))
+               pr.iterations.copy(), pr.grad_norm.copy(), r.best, r.converged_count,
+               r.pso_best_before_bfgs, lo))
     finally:
         dist.destroy_process_group()
 
 
-def _run(case, world=2):
+def _run(case, world=2, gather="root"):
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, case)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, case, gather))
+             for r in range(world)]
     for p in procs:
         p.start()
     out = sorted((q.get(timeout=600) for _ in range(world)), key=lambda t: t[0])
@@ -103,19 +105,27 @@ def _run(case, world=2):
     return out
 
 
-@pytest.mark.parametrize("case", ["shard", "shard_peer"])
-def test_two_process_run_is_bit_identical_to_one(z, case):
-    """`shard_peer`: the per-sweep barrier runs inside the sweep kernels as a
-    peer-memory exchange between the two processes (IPC-mapped blocks,
-    system-scope release/acquire flags) instead of the all-gather."""
+@pytest.mark.parametrize("case,world,gather", [("shard", 2, "all"), ("shard_peer", 2, "all"),
+                                               ("shard", 4, "root"), ("shard_peer", 4, "root")])
+def test_multi_process_run_is_bit_identical_to_one(z, case, world, gather):
+    """2 and 4 processes on the one GPU: per_run, best, tallies and the PSO
+    best bit-identical to the one-process run.  `shard_peer`: the per-sweep
+    barrier runs inside the sweep kernels as a peer-memory exchange between
+    the processes (IPC-mapped blocks, system-scope release/acquire flags)
+    instead of the all-gather.  gather="all": every rank holds all N
+    outcomes; gather="root" (the default): rank 0 holds all N, every other
+    rank its own shard, and every rank the global best."""
     fn, cfg = _cfg(z, "shard")
     one = z.zeus_run(fn, cfg)
-    for rank, x, f, s, k, gn, bf, conv, psob in _run(case):
-        assert np.array_equal(x, one.per_run.x_final), rank
-        assert np.array_equal(f, one.per_run.f_final, equal_nan=True)
-        assert np.array_equal(s, one.per_run.status_codes)
-        assert np.array_equal(k, one.per_run.iterations)
-        assert bf == one.best.f_final and conv == one.converged_count
+    for rank, x, f, s, k, gn, best, conv, psob, lo in _run(case, world, gather):
+        full = gather == "all" or rank == 0
+        sl = slice(0, cfg.N) if full else slice(lo, lo + len(s))
+        assert full == (len(s) == cfg.N), (rank, len(s))
+        assert np.array_equal(x, one.per_run.x_final[sl]), rank
+        assert np.array_equal(f, one.per_run.f_final[sl], equal_nan=True)
+        assert np.array_equal(s, one.per_run.status_codes[sl])
+        assert np.array_equal(k, one.per_run.iterations[sl])
+        assert best == one.best and conv == one.converged_count
         assert psob == one.pso_best_before_bfgs
 
 
@@ -129,7 +139,8 @@ def test_two_process_early_stop_semantics(z):
     fn, cfg = _cfg(z, "stop")
     out = _run("stop")
     r0, r1 = out
-    assert np.array_equal(r0[3], r1[3])          # both ranks see the same gathered per_run
+    assert np.array_equal(r0[3][r1[9]:], r1[3])  # rank 1 holds its shard of rank 0's table
+    assert r0[6] == r1[6]                        # the same global best on both ranks
     x, f, s, k, gn, bf, conv = r0[1], r0[2], r0[3], r0[4], r0[5], r0[6], r0[7]
     assert len(s) == cfg.N                        # parallel mode: every start reported
     assert conv == int(np.sum(s == 0)) and conv >= cfg.required_c

@@ -159,8 +159,40 @@ def disagreements(a_s, a_x, a_gn, b_s, b_x, b_gn):
     return flips, basins
 
 
-def gate(label, dev, ref, floor_count):
-    """The bar stated in the module docstring; returns the report."""
+def perturbed_starts(x0, k, seed=0):
+    """k copies of x0, each coordinate moved by -1, 0 or +1 ulp at random."""
+    rng = np.random.default_rng(seed)
+    steps = rng.integers(-1, 2, size=(k, len(x0)))
+    up, dn = np.nextafter(x0, np.inf), np.nextafter(x0, -np.inf)
+    return np.where(steps > 0, up, np.where(steps < 0, dn, x0))
+
+
+def certify(oracle, name, x0, cap, dev_status, dev_x, k=64):
+    """Rounding-level certificate for a start on which two implementations
+    disagree: run the ORACLE from k starts within 1 ulp of x0.  Returns
+    'reached' when one of those runs ends with the device's status at the
+    device's minimiser (|dx| <= 1e-6), 'unstable' when the oracle's own
+    outcome changes under the perturbations (status or |dx| > 1e-6), else
+    None -- a disagreement no rounding-level change of the start explains."""
+    r = oracle.bfgs_batch(name, perturbed_starts(np.asarray(x0, dtype=np.float64), k),
+                          iter_bfgs=cap)
+    dx_dev = np.max(xdiff(r.x_final, np.asarray(dev_x)[None, :]), axis=1)
+    if np.any((r.status == dev_status) & (dx_dev <= 1e-6)):
+        return "reached"
+    base = oracle.bfgs_batch(name, np.asarray(x0, dtype=np.float64)[None, :], iter_bfgs=cap)
+    dx_base = np.max(xdiff(r.x_final, base.x_final), axis=1)
+    if np.any((r.status != base.status[0]) | (dx_base > 1e-6)):
+        return "unstable"
+    return None
+
+
+def gate(label, dev, ref, floor_count, cert=None):
+    """The full-size parity bar (tests/test_gpu_parity_fullsize.py):
+    agreeing starts within the stated tolerance; every status flip a start
+    stalled near theta on both sides; the number of disagreements (flips +
+    different minima) at most 2 x the oracle-vs-reference noise floor + 2;
+    and, with ``cert = (oracle, name, starts, cap)``, every disagreement
+    certified at the rounding level (certify())."""
     rep = parity_report(label, dev.x_final, dev.f_final, dev.grad_norm, dev.iterations,
                         dev.status_codes, ref)
     flips, basins = disagreements(dev.status_codes, dev.x_final, dev.grad_norm,
@@ -176,6 +208,16 @@ def gate(label, dev, ref, floor_count):
     gmax = np.maximum(dev.grad_norm[flips], np.asarray(ref.grad_norm)[flips])
     assert np.all(gmax < FLOOR_GN), (label, flips[gmax >= FLOOR_GN][:10])
     assert n_dis <= allowed, (label, n_dis, allowed)
+    if cert is not None and n_dis:
+        oracle, name, starts, cap = cert
+        verdicts = {}
+        for i in np.concatenate([flips, basins]):
+            v = certify(oracle, name, starts[i], cap, int(dev.status_codes[i]), dev.x_final[i])
+            verdicts[v] = verdicts.get(v, 0) + 1
+            assert v is not None, (label, "uncertified disagreement at start", int(i))
+        print(f"[parity] {label}: rounding-level certificates {verdicts} (oracle from starts "
+              f"within 1 ulp: 'reached' = lands on the device's outcome)")
+        rep["certificates"] = verdicts
     keep = np.ones(len(dev.status_codes), dtype=bool)
     keep[flips] = False
     keep[basins] = False
@@ -184,5 +226,3 @@ def gate(label, dev, ref, floor_count):
                           label, np.asarray(ref.grad_norm)[keep])
     rep["disagreements"] = n_dis
     return rep
-
-

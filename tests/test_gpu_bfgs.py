@@ -103,7 +103,7 @@ def test_wide_kernel_shapes_match_oracle(oracle, name, d, n):
         x_final, f_final, grad_norm = dev["x"], dev["f"], dev["gn"]
         iterations, status_codes = dev["k"], dev["s"]
 
-    gate(f"wide {name} d={d}", D, ref, 0)
+    gate(f"wide {name} d={d}", D, ref, 0, cert=(oracle, name, starts, 2000))
 
 
 def test_hand_traces(z, golden):

@@ -171,11 +171,12 @@ def test_bench_two_ranks_prints_one_line(exchange):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
            "--gpus", "2", "--config", "c1", "--steps", "2", "--warmup", "3",
-           "--no-cpu-baseline", "--no-north-star"]
+           "--no-cpu-baseline"]
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "start-sharded x2"
+    assert d["gpu_launches"] > 0 and d["roofline"]["achieved"] > 0
     assert d["value"] > 0 and d["e2e"]["value"] > 0

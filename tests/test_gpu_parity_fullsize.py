@@ -112,7 +112,7 @@ def test_against_reference_fixtures(z, oracle, tag):
     print(f"\n[parity] {tag}: oracle vs reference: {len(f_o)} flips, {len(b_o)} different "
           f"minima of {len(g.idx)}")
     gate(f"{tag} device vs reference ({len(g.idx)} starts of {g.n})", Sub(res.per_run, g.idx), g,
-         len(f_o) + len(b_o))
+         len(f_o) + len(b_o), cert=(oracle, g.name, g.x0, g.cap))
 
 
 @pytest.mark.parametrize("name,d,n,sweeps,cap,seed", [
@@ -132,7 +132,7 @@ def test_small_configs_every_start_vs_oracle(z, oracle, name, d, n, sweeps, cap,
     assert res.pso_best_before_bfgs == pso_best
     # config 2's oracle-vs-reference floor: 2 flips in 8,192 (fixture c2) -> 16 per 65,536
     rep = gate(f"{name} d={d} N={n} device vs oracle", Sub(res.per_run), ref,
-               0 if d == 2 else 16)
+               0 if d == 2 else 16, cert=(oracle, name, sw.positions, cap))
     assert abs(res.converged_count - conv) <= rep["flips"]
     assert abs(res.best.f_final - ref.f_final[best]) <= 1e-10 * max(1, abs(ref.f_final[best]))
 
@@ -157,7 +157,7 @@ def test_wide_configs_vs_oracle(z, oracle, name, d, n, sweeps, cap, stride, floo
                                            iter_bfgs=cap, seed=42, deterministic=True))
     assert res.pso_best_before_bfgs == sw.global_best_val
     gate(f"{name} d={d} N={n} device vs oracle ({len(idx)} strided)", Sub(res.per_run, idx), ref,
-         floor)
+         floor, cert=(oracle, name, sw.positions[idx], cap))
 
 
 @pytest.mark.parametrize("sweeps,cap", [(20, 2000), (0, 2000), (5, 1024), (5, 128), (100, 16)])
@@ -175,4 +175,4 @@ def test_config5_every_start_vs_oracle(z, oracle, sweeps, cap):
                                                iter_bfgs=cap, seed=42, deterministic=True))
     floor = {16: 35 * 4}.get(cap, 4)
     gate(f"c5 rastrigin d=20 sweeps={sweeps} cap={cap} device vs oracle", Sub(res.per_run), ref,
-         floor)
+         floor, cert=(oracle, "rastrigin", sw.positions, cap))

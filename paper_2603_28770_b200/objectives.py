@@ -139,9 +139,9 @@ def objective_id(f, dim: int | None = None):
 
     Accepts this package's functions, ``ObjectiveSpec`` objects, registry
     names, and the reference package's own functions (matched by module and
-    name, ``zeus.objectives.<name>``).  Anything else raises
-    ``NotImplementedError``: kernels cannot run Python and there is no CPU
-    fallback.  Goldstein-Price at ``dim != 2`` raises ``ValueError`` like the
+    name, ``zeus.objectives.<name>``).  Any other callable is a user
+    objective: with ``dim`` it is traced into a DeviceObjective (trace.py);
+    kernels cannot run Python and there is no CPU fallback.  Goldstein-Price at ``dim != 2`` raises ``ValueError`` like the
     reference's evaluation would (objectives.py:92-93).
     """
     from .plugin import DeviceObjective
@@ -166,10 +166,17 @@ def objective_id(f, dim: int | None = None):
             cand = getattr(f, "__name__", None)
             name = cand if cand in _REGISTRY else None
     if name is None:
+        if callable(f) and dim is not None:
+            # a generic Python objective (pkg/README.md:70-87): traced once into
+            # device source and compiled with NVRTC (trace.py); a callable that
+            # cannot be traced raises TraceError (a NotImplementedError)
+            from .trace import traced_objective
+
+            return traced_objective(f, int(dim))
         raise NotImplementedError(
             f"objective {getattr(f, '__name__', f)!r} is not a registered device objective "
-            f"({', '.join(objective_names())}); user-defined objectives need a device "
-            f"plug-in (DESIGN.md, 'next'), there is no CPU fallback")
+            f"({', '.join(objective_names())}) and no dimension was given to trace it; "
+            f"there is no CPU fallback")
     if name == "goldstein_price" and dim is not None and dim != 2:
         raise ValueError("goldstein_price is defined for exactly 2 dimensions")
     return int(_REGISTRY[name]["obj_id"])

@@ -44,6 +44,23 @@ class ParticleStreams:
     def advance_all(self, count: int) -> None:
         self._offset += count
 
+    def generator(self, i: int) -> np.random.Generator:
+        """Particle i's stream as a numpy Generator (streams.py:32-39):
+        ``Generator(Philox(key=[seed, i]))`` positioned at this family's
+        current draw offset for particle i.  The kernels regenerate draws
+        from (seed, i, k) on the device, so this is a host VIEW of the same
+        stream: draws taken from it do not advance the family's offset (the
+        reference's object is the stream itself)."""
+        if not 0 <= i < self.n:
+            raise IndexError(i)
+        key = np.array([self.seed, i], dtype=np.uint64)
+        bitgen = np.random.Philox(key=key)
+        off = int(self._offset[i])
+        bitgen.advance(off // 4)         # whole 4-word blocks
+        if off % 4:
+            bitgen.random_raw(off % 4)   # into the block
+        return np.random.Generator(bitgen)
+
     def draw_uniform(self, i: int, low: float, high: float, size: int) -> np.ndarray:
         """Next ``size`` uniforms in [low, high) from particle i's stream."""
         if not 0 <= i < self.n:

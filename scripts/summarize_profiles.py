@@ -1,15 +1,23 @@
 """Turn one gpurun call's ncu output into committed summaries under profiles/.
 
-    python scripts/summarize_profiles.py <gpurun_out dir> <tag> [--config c2]
+    python scripts/summarize_profiles.py <tag> --config t50 [--rep R.ncu-rep ...]
+                                          [--launches launches.csv]
 
 Writes
-  profiles/<tag>_launches.txt   per-kernel totals of the launch list
+  profiles/<tag>_<config>_launches.txt  per-kernel totals of the launch list
                                 (ncu --metrics gpu__time_duration.sum
-                                --clock-control none), with each kernel's share
-  profiles/<tag>_ncu_<kernel>.txt  key metrics of each `ncu --set full` capture
-                                (FP64 pipe, issue, DRAM bytes, stalls)
-  profiles/ncu_summary.json     {config: {kernel, dram_bytes_per_launch, ...}}
-                                read by bench.py for roofline.traffic
+                                --clock-control none) of one bench step of the
+                                config, with each kernel's share
+  profiles/<tag>_<config>_ncu_<kernel>.txt  key metrics of each `ncu --set
+                                full` capture (FP64 pipe, issue, DRAM bytes,
+                                stalls)
+  profiles/ncu_summary.json     {config: {"kernels": {"<objective><d>":
+                                {dram_bytes_per_launch, kernels, sources}}}}
+                                read by bench.py for roofline.traffic: each
+                                BFGS capture is keyed by the config's problem
+                                with that objective (the small-d tiers of one
+                                problem are summed: one zeus_run launches
+                                them in sequence)
 """
 
 from __future__ import annotations
@@ -93,34 +101,38 @@ def to_bytes(v, unit):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("src")
     ap.add_argument("tag")
-    ap.add_argument("--config", default="c2")
-    ap.add_argument("--launches", default="launches.csv")
+    ap.add_argument("--config", required=True)
+    ap.add_argument("--rep", nargs="*", default=[])
+    ap.add_argument("--launches", default=None)
     args = ap.parse_args()
+    sys.path.insert(0, ROOT)
+    from bench import CONFIGS
+
+    probs = CONFIGS[args.config]["problems"]
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
-    lp = os.path.join(args.src, args.launches)
-    if os.path.exists(lp):
-        agg = launches(lp)
+    base = f"{args.tag}_{args.config}"
+    if args.launches and os.path.exists(args.launches):
+        agg = launches(args.launches)
         # bench.py's DFMA peak probe runs before the timed steps: not part of a step
-        agg = collections.OrderedDict((k, v) for k, v in agg.items() if "dfma_peak" not in k)
+        agg = collections.OrderedDict((k, v) for k, v in agg.items() if "dfma" not in k)
         tot = sum(v[1] for v in agg.values())
-        lines = [f"# {args.tag}: ncu --metrics gpu__time_duration.sum --clock-control none "
-                 f"(cold-cache, serialised; shares, not absolutes, are comparable)",
+        lines = [f"# {base}: ncu --metrics gpu__time_duration.sum --clock-control none of one "
+                 f"bench.py step (cold-cache, serialised; shares, not absolutes, compare)",
                  f"# {'launches':>8} {'total_us':>12} {'share':>6}  kernel"]
         for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             lines.append(f"  {n:8d} {t:12.1f} {100 * t / tot:5.1f}%  {k}")
-        open(os.path.join(prof, f"{args.tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
+        open(os.path.join(prof, f"{base}_launches.txt"), "w").write("\n".join(lines) + "\n")
         print("\n".join(lines))
     summ_path = os.path.join(prof, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
-    fresh = {}
-    for rep in sorted(glob.glob(os.path.join(args.src, "*.ncu-rep"))):
+    entry = {"kernels": {}}
+    for rep in args.rep:
         for m in raw_metrics(rep):
             kname = m["kernel"].split("(")[0]
             short = kname.replace("void ", "").replace("zeus::", "")
-            lines = [f"# {args.tag}: ncu --set full --clock-control none of {short}",
+            lines = [f"# {base}: ncu --set full --clock-control none of {short}",
                      f"grid {m['grid']} block {m['block']}"]
             for k in KEYS:
                 if k in m:
@@ -128,22 +140,25 @@ def main():
             lines.append("top stalls (warps per issue-active cycle): " +
                          ", ".join(f"{k} {v:.3f}" for k, v in m["stalls"].items()))
             safe = "".join(c if c.isalnum() else "_" for c in short)[:60].strip("_")
-            fn = os.path.join(prof, f"{args.tag}_ncu_{safe}.txt")
+            fn = os.path.join(prof, f"{base}_ncu_{safe}.txt")
             open(fn, "w").write("\n".join(lines) + "\n")
-            try:
-                print("\n".join(lines))
-            except BrokenPipeError:
-                pass
-            if "dram__bytes_read.sum" in m and short.startswith("bfgs"):
-                # the BFGS tiers of one step together (bench.py's roofline spans them)
-                rd = to_bytes(*m["dram__bytes_read.sum"])
-                wr = to_bytes(*m["dram__bytes_write.sum"])
-                e = fresh.setdefault(args.config, {"kernels": [], "dram_bytes_per_launch": 0.0,
-                                                   "sources": []})
-                e["kernels"].append(short)
-                e["dram_bytes_per_launch"] += rd + wr
-                e["sources"].append(os.path.basename(fn))
-    summ.update(fresh)
+            print("\n".join(lines))
+            if "dram__bytes_read.sum" not in m or not short.startswith("bfgs"):
+                continue
+            obj = short[short.index("<") + 1:].split(",")[0].split(">")[0].strip().lower()
+            match = [p for p in probs if p["obj"] == obj]
+            if len(match) != 1:
+                continue
+            key = f"{obj}{match[0]['d']}"
+            rd = to_bytes(*m["dram__bytes_read.sum"])
+            wr = to_bytes(*m["dram__bytes_write.sum"])
+            e = entry["kernels"].setdefault(key, {"dram_bytes_per_launch": 0.0, "kernels": [],
+                                                  "sources": []})
+            e["kernels"].append(short)
+            e["dram_bytes_per_launch"] += rd + wr
+            e["sources"].append(os.path.basename(fn))
+    if entry["kernels"]:
+        summ[args.config] = entry
     json.dump(summ, open(summ_path, "w"), indent=1)
 
 

@@ -52,9 +52,12 @@ def test_public_namespace_matches_reference():
                      "objective_names", "ZeusConfig", "ZeusResult", "zeus_run", "reduce_best",
                      "make_start_streams", "NoValidOptimumError", "__version__"]
     missing = [n for n in reference_all if not hasattr(z, n)]
-    # Dual is the host-side scalar type for user objectives: out of scope
-    # until the device objective plug-in exists.
-    assert missing == ["Dual"]
+    assert missing == []
+    from paper_2603_28770_b200 import autodiff
+
+    for n in ("Dual", "DomainError", "exp", "cos", "sin", "sqrt", "log", "powf",
+              "forward_gradient"):   # zeus/autodiff.py:19-29
+        assert hasattr(autodiff, n), n
     assert (z.CONVERGED, z.DIVERGED, z.STOPPED, z.DOMAIN_ERROR) == (
         "converged", "diverged", "stopped", "domain_error")
 

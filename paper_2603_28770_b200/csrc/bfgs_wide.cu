@@ -16,7 +16,8 @@
 // rows of the two inverse-Hessian columns H[:, c0], H[:, c1]; rows RR..d-1 of
 // those columns live in the start's shared-memory slice (conflict-free: lanes
 // read consecutive columns).  The per-row broadcast values of the fused H
-// pass {dg_i, g'_i, dx_i, u_i} are the only other shared-memory traffic.
+// pass {g'_i, dx_i, u_i} (three [64 W] arrays, read two rows per 16-byte
+// load) are the only other shared-memory traffic.
 //
 // Per iteration (reference order, bfgs.py:108-156):
 //  1. Armijo search (linesearch.py:60-71) in chunks of CH trials
@@ -45,15 +46,6 @@ namespace zeus {
 namespace {
 
 constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
-
-#ifndef ZEUS_WIDE_UFROMP
-#define ZEUS_WIDE_UFROMP 1
-#endif
-#if ZEUS_WIDE_UFROMP
-#define UACC(x)
-#else
-#define UACC(x) x
-#endif
 
 // Term j's coordinate accessor: x(j) -> xj, x(j + 1) -> xj1 (Rosenbrock's
 // neighbour); objectives only ever ask for these two.
@@ -109,19 +101,22 @@ struct WideShape {
 #endif
 };
 
-// Shared-memory slice of one start, in doubles: rowv [64W][4], H rows
+// Shared-memory slice of one start, in doubles: rowv [4][64W] (g', dx, u and
+// a spare row), H rows
 // [d - RR][64W], exchange scratch (W > 1): two reduction buffers [2][W][8],
 // boundary values x, p, tangent [3][W].
 __host__ __device__ inline int wide_slot_doubles(int d, int rr, int w) {
   return 4 * 64 * w + (d > rr ? d - rr : 0) * 64 * w + (w > 1 ? 16 * w + 3 * w : 0);
 }
 
-template <class Obj, int RR, int W>
+// D > 0: the kernel compiled for that dimension (row loops fully unrolled,
+// shared-memory offsets immediate); D = 0: any 32 < d <= 64 W at run time.
+template <class Obj, int RR, int W, int D>
 struct WideStart {
   static constexpr int NA = Obj::NACC;
   static constexpr int LD = 64 * W;  // row stride of the shared-memory H rows
   double* Hs;          // [d - RR][LD] rows RR.. of every column of the start
-  double* rowv;        // [64 W][4] {dg, g', dx_prev, u_prev}
+  double* rowv;        // [4][64 W]: g' | dx_prev | u_prev | (unused)
   double* xch;         // W > 1: [2][W][8] reductions, then xb[W], pb[W], tb[W]
   const double* atab;  // block alpha table
   int wi = 0;          // warp index within the start (0 .. W-1)
@@ -322,7 +317,7 @@ struct WideStart {
   }
 
   __device__ void run(const BfgsArgs& A, long long s, int l) {
-    const int d = A.d;
+    const int d = D > 0 ? D : A.d;
     const int nt = Obj::nterms(d);
     const int c0 = 64 * wi + l, c1 = c0 + 32;
     const bool own0 = W == 1 || c0 < d, own1 = c1 < d;
@@ -347,9 +342,9 @@ struct WideStart {
       Hs[(i - RR) * LD + c1] = i == c1 ? 1.0 : 0.0;
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      rowv[4 * c0 + q] = 0.0;
-      rowv[4 * c1 + q] = 0.0;
+    for (int q = 0; q < 3; ++q) {
+      rowv[q * LD + c0] = 0.0;
+      rowv[q * LD + c1] = 0.0;
     }
     if (own0) x0 = A.x0[(int64_t)c0 * A.ldx + s];
     if (own1) x1 = A.x0[(int64_t)c1 * A.ldx + s];
@@ -483,92 +478,87 @@ struct WideStart {
         }
       }
       const double dg0 = gn0 - g0, dg1 = gn1 - g1;
-      if (own0) reinterpret_cast<double2*>(rowv + 4 * c0)[0] = make_double2(dg0, gn0);
-      if (own1) reinterpret_cast<double2*>(rowv + 4 * c1)[0] = make_double2(dg1, gn1);
+      if (own0) rowv[c0] = gn0;
+      if (own1) rowv[c1] = gn1;
       team_sync();
 
-      // ---- fused pass over my two columns: lazy update, w = H g' (u = w + p).
+      // ---- fused pass over my two columns: the lazy rank-2 update of the
+      // previous iteration (coefficients zero when its curvature guard
+      // skipped it: no select in the pass) and w = H g' (u = w + p below).
       // Four accumulators per column (rows i mod 4) so a warp keeps 8
-      // independent DFMA chains in flight (FP64 latency ~23 cycles).
+      // independent DFMA chains in flight; rows come in pairs, one 16-byte
+      // load of each of g', dx, u per pair.
       double u0 = 0.0, w0 = 0.0, u1 = 0.0, w1 = 0.0;
       {
+        const double* G = rowv;
+        const double* DX = rowv + LD;
+        const double* U = rowv + 2 * LD;
         double wa[4] = {0.0, 0.0, 0.0, 0.0}, wb[4] = {0.0, 0.0, 0.0, 0.0};
-        double ua[4] = {0.0, 0.0, 0.0, 0.0}, ub[4] = {0.0, 0.0, 0.0, 0.0};
+        static_assert(RR % 2 == 0, "register rows in pairs");
 #pragma unroll
-        for (int i = 0; i < RR; ++i) {
-          const double2 ra = *reinterpret_cast<const double2*>(rowv + 4 * i);      // dg, g'
-          const double2 rb = *reinterpret_cast<const double2*>(rowv + 4 * i + 2);  // dx, u
-          const double e0 = pending ? fma(rb.x, a0, fma(rb.y, b0, h0[i])) : h0[i];
-          const double e1 = pending ? fma(rb.x, a1, fma(rb.y, b1, h1[i])) : h1[i];
-          h0[i] = e0;
-          h1[i] = e1;
-          UACC(ua[i & 3] = fma(e0, ra.x, ua[i & 3]));
-          wa[i & 3] = fma(e0, ra.y, wa[i & 3]);
-          UACC(ub[i & 3] = fma(e1, ra.x, ub[i & 3]));
-          wb[i & 3] = fma(e1, ra.y, wb[i & 3]);
+        for (int i = 0; i < RR; i += 2) {
+          const double2 g2 = *reinterpret_cast<const double2*>(G + i);
+          const double2 x2 = *reinterpret_cast<const double2*>(DX + i);
+          const double2 u2 = *reinterpret_cast<const double2*>(U + i);
+          h0[i] = fma(x2.x, a0, fma(u2.x, b0, h0[i]));
+          h1[i] = fma(x2.x, a1, fma(u2.x, b1, h1[i]));
+          h0[i + 1] = fma(x2.y, a0, fma(u2.y, b0, h0[i + 1]));
+          h1[i + 1] = fma(x2.y, a1, fma(u2.y, b1, h1[i + 1]));
+          wa[i & 3] = fma(h0[i], g2.x, wa[i & 3]);
+          wb[i & 3] = fma(h1[i], g2.x, wb[i & 3]);
+          wa[(i + 1) & 3] = fma(h0[i + 1], g2.y, wa[(i + 1) & 3]);
+          wb[(i + 1) & 3] = fma(h1[i + 1], g2.y, wb[(i + 1) & 3]);
         }
-        // rows RR.. from shared memory, four per step with every load issued
+        // rows RR.. from shared memory, SR per step with every load issued
         // before the arithmetic (the loads' latency overlaps)
-        int i = RR;
         constexpr int SR = WideShape<Obj, W>::SR;  // shared-memory rows per step
-        static_assert(SR >= 1 && SR <= 4, "four accumulators per column");
-        for (; i + SR - 1 < d; i += SR) {
-          double2 ra[SR], rb[SR];
+        static_assert(SR == 2 || SR == 4, "rows in pairs, four accumulators per column");
+        int i = RR;
+#pragma unroll
+        for (; i + SR - 1 < (D > 0 ? D : d); i += SR) {
+          double2 g2[SR / 2], x2[SR / 2], u2[SR / 2];
           double e0[SR], e1[SR];
           double* hr = Hs + (i - RR) * LD;
 #pragma unroll
+          for (int r = 0; r < SR / 2; ++r) {
+            g2[r] = *reinterpret_cast<const double2*>(G + i + 2 * r);
+            x2[r] = *reinterpret_cast<const double2*>(DX + i + 2 * r);
+            u2[r] = *reinterpret_cast<const double2*>(U + i + 2 * r);
+          }
+#pragma unroll
           for (int r = 0; r < SR; ++r) {
-            ra[r] = *reinterpret_cast<const double2*>(rowv + 4 * (i + r));
-            rb[r] = *reinterpret_cast<const double2*>(rowv + 4 * (i + r) + 2);
             e0[r] = hr[r * LD + c0];
             e1[r] = hr[r * LD + c1];
           }
-          if (pending) {
-#pragma unroll
-            for (int r = 0; r < SR; ++r) {
-              e0[r] = fma(rb[r].x, a0, fma(rb[r].y, b0, e0[r]));
-              e1[r] = fma(rb[r].x, a1, fma(rb[r].y, b1, e1[r]));
-              hr[r * LD + c0] = e0[r];
-              hr[r * LD + c1] = e1[r];
-            }
-          }
 #pragma unroll
           for (int r = 0; r < SR; ++r) {
-            UACC(ua[r] = fma(e0[r], ra[r].x, ua[r]));
-            wa[r] = fma(e0[r], ra[r].y, wa[r]);
-            UACC(ub[r] = fma(e1[r], ra[r].x, ub[r]));
-            wb[r] = fma(e1[r], ra[r].y, wb[r]);
+            const double xr = (r & 1) ? x2[r / 2].y : x2[r / 2].x;
+            const double ur = (r & 1) ? u2[r / 2].y : u2[r / 2].x;
+            const double gr = (r & 1) ? g2[r / 2].y : g2[r / 2].x;
+            e0[r] = fma(xr, a0, fma(ur, b0, e0[r]));
+            e1[r] = fma(xr, a1, fma(ur, b1, e1[r]));
+            hr[r * LD + c0] = e0[r];
+            hr[r * LD + c1] = e1[r];
+            wa[r] = fma(e0[r], gr, wa[r]);
+            wb[r] = fma(e1[r], gr, wb[r]);
           }
         }
-        for (; i < d; ++i) {
-          const double2 ra = *reinterpret_cast<const double2*>(rowv + 4 * i);
-          const double2 rb = *reinterpret_cast<const double2*>(rowv + 4 * i + 2);
+#pragma unroll 1
+        for (; i < (D > 0 ? D : d); ++i) {  // (the < SR remainder rows)
           double* hr = Hs + (i - RR) * LD;
-          double e0 = hr[c0], e1 = hr[c1];
-          if (pending) {
-            e0 = fma(rb.x, a0, fma(rb.y, b0, e0));
-            e1 = fma(rb.x, a1, fma(rb.y, b1, e1));
-            hr[c0] = e0;
-            hr[c1] = e1;
-          }
-          UACC(ua[0] = fma(e0, ra.x, ua[0]));  // (the < SR remainder rows)
-          wa[0] = fma(e0, ra.y, wa[0]);
-          UACC(ub[0] = fma(e1, ra.x, ub[0]));
-          wb[0] = fma(e1, ra.y, wb[0]);
+          const double e0 = fma(DX[i], a0, fma(U[i], b0, hr[c0]));
+          const double e1 = fma(DX[i], a1, fma(U[i], b1, hr[c1]));
+          hr[c0] = e0;
+          hr[c1] = e1;
+          wa[0] = fma(e0, G[i], wa[0]);
+          wb[0] = fma(e1, G[i], wb[0]);
         }
         w0 = (wa[0] + wa[1]) + (wa[2] + wa[3]);
         w1 = (wb[0] + wb[1]) + (wb[2] + wb[3]);
-#if ZEUS_WIDE_UFROMP
         // u = H_k dg = H_k g' - H_k g = w + p: p = -H_k g is this iteration's
         // direction (exact in exact arithmetic), so the pass needs one matvec
         u0 = w0 + p0;
         u1 = w1 + p1;
-        (void)ua;
-        (void)ub;
-#else
-        u0 = (ua[0] + ua[1]) + (ua[2] + ua[3]);
-        u1 = (ub[0] + ub[1]) + (ub[2] + ub[3]);
-#endif
         if (!own0) u0 = w0 = 0.0;
         if (!own1) u1 = w1 = 0.0;
       }
@@ -595,6 +585,8 @@ struct WideStart {
         const double cc = pending ? fma(rho * rho, part[4], rho) : 0.0;
         const double ug = part[5], xg = part[6];
         double q0 = -w0, q1 = -w1;
+        a0 = b0 = a1 = b1 = 0.0;  // skipped update (bfgs.py:69-71): the pass adds 0
+        double rx0 = 0.0, ru0 = 0.0, rx1 = 0.0, ru1 = 0.0;
         if (pending) {
           // p' = -(w - rho dx (u.g') - rho u (dx.g') + c dx (dx.g'))
           q0 = -(w0 + fma(dx0, fma(cc, xg, -rho * ug), -rho * xg * u0));
@@ -603,8 +595,15 @@ struct WideStart {
           b0 = -rho * dx0;
           a1 = fma(cc, dx1, -rho * u1);
           b1 = -rho * dx1;
-          if (own0) reinterpret_cast<double2*>(rowv + 4 * c0)[1] = make_double2(dx0, u0);
-          if (own1) reinterpret_cast<double2*>(rowv + 4 * c1)[1] = make_double2(dx1, u1);
+          rx0 = dx0, ru0 = u0, rx1 = dx1, ru1 = u1;
+        }
+        if (own0) {
+          rowv[LD + c0] = rx0;
+          rowv[2 * LD + c0] = ru0;
+        }
+        if (own1) {
+          rowv[LD + c1] = rx1;
+          rowv[2 * LD + c1] = ru1;
         }
         if (!own0) q0 = 0.0;
         if (!own1) q1 = 0.0;
@@ -650,7 +649,7 @@ struct WideStart {
   }
 };
 
-template <class Obj, int RR, int W>
+template <class Obj, int RR, int W, int D>
 __global__ void __launch_bounds__(kWideThreads, WideShape<Obj, W>::MINB)
     bfgs_wide_kernel(BfgsArgs A) {
   extern __shared__ double sm[];
@@ -664,7 +663,7 @@ __global__ void __launch_bounds__(kWideThreads, WideShape<Obj, W>::MINB)
     }
   }
   __syncthreads();
-  WideStart<Obj, RR, W> S;
+  WideStart<Obj, RR, W, D> S;
   const int start_slot = wib / W;  // W = 1: two independent starts per block
   S.wi = wib % W;
   S.atab = alpha_tab;
@@ -690,14 +689,14 @@ __global__ void __launch_bounds__(kWideThreads, WideShape<Obj, W>::MINB)
 
 namespace {
 
-template <class Obj, int RR, int W>
+template <class Obj, int RR, int W, int D>
 int launch_wide(BfgsArgs A, cudaStream_t s) {
   A.nalpha = kAlphaTable;
   A.warp_doubles = wide_slot_doubles(A.d, RR, W);  // per start
   const int starts_per_block = 2 / W;
   const size_t smem =
       sizeof(double) * ((size_t)A.nalpha + (size_t)starts_per_block * A.warp_doubles);
-  auto kern = bfgs_wide_kernel<Obj, RR, W>;
+  auto kern = bfgs_wide_kernel<Obj, RR, W, D>;
   int rc = check_cuda(
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
       "cudaFuncSetAttribute(wide)");
@@ -727,8 +726,12 @@ struct WideLaunch {
     if constexpr (Obj::kId == ZEUS_OBJ_GOLDSTEIN_PRICE) {
       return set_error(ZEUS_ERR_UNSUPPORTED, "wide: goldstein_price is 2-D");
     } else {
-      if (A.d <= 64) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1>(A, s);
-      return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2>(A, s);
+      // the BASELINE dimensions get kernels compiled for them (T50: d = 50;
+      // config 4: d = 100); any other 32 < d <= 128 runs the generic build
+      if (A.d == 50) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 50>(A, s);
+      if (A.d <= 64) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 0>(A, s);
+      if (A.d == 100) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2, 100>(A, s);
+      return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2, 0>(A, s);
     }
   }
 };

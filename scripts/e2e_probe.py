@@ -1,29 +1,18 @@
-"""Where config 2's end-to-end time goes beyond the device time: wall vs
-device per zeus_run with the bench's L2 flush, with / without the NVML clock
-sampler thread, and a per-section host timeline of one call."""
+"""Wall vs device time of config-2 zeus_run calls (the bench's L2 flush between
+calls): how much of the end-to-end time lies outside the device window."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, '.')
 import numpy as np, torch
 import paper_2603_28770_b200 as z
-import bench
-
-cfg = lambda s: z.ZeusConfig(N=65536, dim=10, range=(-5.12, 5.12), iter_pso=20, iter_bfgs=2000,
-                             seed=s, deterministic=True)
-dev = torch.device("cuda", 0)
-flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-for s in range(3):
-    z.zeus_run(z.rastrigin, cfg(1000 + s))
-for sampler in (False, True):
-    rows = []
-    ctx = bench.ClockSampler(0) if sampler else None
-    if ctx: ctx.__enter__()
-    for s in range(8):
-        flush.fill_(float(s)); torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r = z.zeus_run(z.rastrigin, cfg(42 + s))
-        t1 = time.perf_counter()
-        rows.append(((t1 - t0) * 1e3, r.wall_time * 1e3, r.device_time * 1e3))
-    if ctx: ctx.__exit__(None, None, None)
-    a = np.array(rows)
-    print("sampler" if sampler else "no sampler", "outer wall %.3f  wall %.3f  device %.3f  gap %.3f ms" %
-          tuple(list(a.mean(0)) + [a[:, 1].mean() - a[:, 2].mean()]))
+cfg = lambda s: z.ZeusConfig(N=65536, dim=10, range=(-5.12, 5.12), iter_pso=20, iter_bfgs=2000, seed=s, deterministic=True)
+for s in range(3): z.zeus_run(z.rastrigin, cfg(1000 + s))
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+rows = []
+for s in range(6):
+    flush.fill_(1.0); torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = z.zeus_run(z.rastrigin, cfg(42 + s))
+    t1 = time.perf_counter()
+    rows.append(((t1 - t0) * 1e3, r.device_time * 1e3, r.stats.pso_time * 1e3, r.stats.bfgs_time * 1e3, r.stats.reduce_time * 1e3))
+a = np.array(rows).mean(0)
+print("wall %.3f device %.3f (pso %.3f bfgs %.3f reduce %.3f) -> outside device window %.3f ms" % (a[0], a[1], a[2], a[3], a[4], a[0] - a[1]))

@@ -146,3 +146,20 @@ def test_ackley_audit_populations():
     for i, f in au.converged_high:
         assert pr[i].status == "converged" and f > 1.0
     assert au.flagged
+
+
+def test_config5_tradeoff_plan_parses():
+    """BASELINE config 5's grid as a harness plan (plans/tradeoff-c5.ini):
+    PSO sweeps {0,5,20,100} x starts 2^10..2^20 x BFGS depth {16,128,1024}."""
+    import os
+
+    from paper_2603_28770_b200 import bench as hb
+
+    path = os.path.join(os.path.dirname(hb.__file__), "plans", "tradeoff-c5.ini")
+    plan = hb.parse_plan(path, 42)
+    assert len(plan.entries) == 72
+    grid = {(e.config.iter_pso, e.config.N, e.config.iter_bfgs) for e in plan.entries}
+    assert grid == {(s, n, k) for s in (0, 5, 20, 100) for n in (2**10, 2**12, 2**14, 2**16,
+                                                                  2**18, 2**20)
+                    for k in (16, 128, 1024)}
+    assert all(e.config.deterministic and e.spec.dim == 20 for e in plan.entries)

@@ -83,6 +83,10 @@ def lib():
                                         ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                         ctypes.c_int, ctypes.POINTER(Outcome), _dp]
+        L.oracle_bfgs_batch_jitter.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _dp,
+                                               ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                               ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                               ctypes.c_int, _u64, ctypes.POINTER(Outcome), _dp]
         L.oracle_zeus_run.restype = _i64
         L.oracle_zeus_run.argtypes = [ctypes.c_int, ctypes.c_int, _i64, _u64, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_int, ctypes.c_double,
@@ -181,15 +185,20 @@ class BfgsResult:
 
 
 def bfgs_batch(obj, x0, theta=1e-6, iter_bfgs=1000, c1=0.3, alpha0=1.0, iter_ls=20,
-               shrink=0.5, threads=None) -> BfgsResult:
+               shrink=0.5, threads=None, jitter_seed=0) -> BfgsResult:
+    """bfgs_run over the rows of x0.  ``jitter_seed`` != 0 selects the
+    rounding-jitter model (zeus_oracle.c): every objective value and gradient
+    component of row i moved by -1/0/+1 ulp from a per-row stream -- used
+    only by the parity certificates, never as a reference outcome."""
     x0 = np.ascontiguousarray(x0, dtype=np.float64)
     n, d = x0.shape
     out = (Outcome * n)()
     xf = np.empty((n, d))
     if threads is None:
         threads = os.cpu_count() or 1
-    lib().oracle_bfgs_batch(_obj(obj), d, n, _p(x0), theta, iter_bfgs, c1, alpha0,
-                            iter_ls, shrink, threads, out, _p(xf))
+    lib().oracle_bfgs_batch_jitter(_obj(obj), d, n, _p(x0), theta, iter_bfgs, c1, alpha0,
+                                   iter_ls, shrink, threads, jitter_seed & (2**64 - 1), out,
+                                   _p(xf))
     arr = np.frombuffer(out, dtype=np.dtype([(f, "f8" if f in ("f_final", "grad_norm")
                                                else "i8") for f, _ in Outcome._fields_]))
     return BfgsResult(xf, arr["f_final"].copy(), arr["grad_norm"].copy(),

@@ -28,6 +28,36 @@
 #include "zeus_oracle.h"
 
 /* ------------------------------------------------------------------------ */
+/* Rounding-jitter model (certificates only, tests/conftest.py certify()).   */
+/* The device path computes every objective value and gradient component    */
+/* within ~1 ulp of the reference (its sincos is <= 1 ulp from glibc, d > 16 */
+/* folds are trees) and updates H by an algebraically identical O(d^2) form */
+/* (bfgs.py:72-77 rounds differently).  With a non-zero jitter seed,         */
+/* oracle_bfgs_batch_jitter moves each objective value, gradient component, */
+/* direction component and updated H element (symmetrically) of start i by  */
+/* -1, 0 or +1 ulp, drawn from a per-start splitmix64 stream: one sample of */
+/* that rounding freedom.  Off (the default) the oracle is the exact        */
+/* restatement.                                                             */
+/* ------------------------------------------------------------------------ */
+static __thread uint64_t jit_state; /* 0: off */
+
+static inline uint64_t splitmix64(uint64_t *s) {
+  uint64_t z = (*s += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+static inline double jitter(double v) {
+  if (!jit_state || !isfinite(v)) return v;
+  switch (splitmix64(&jit_state) & 3u) {
+    case 1: return nextafter(v, INFINITY);
+    case 2: return nextafter(v, -INFINITY);
+    default: return v;
+  }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Philox4x64-10 (numpy bit generator used by streams.py:36-45)             */
 /* ------------------------------------------------------------------------ */
 
@@ -384,7 +414,7 @@ double oracle_armijo(int obj, int d, const double *x, const double *p,
   double alpha = alpha0;
   for (int k = 0; k < iter_ls + 1; ++k) {
     for (int j = 0; j < d; ++j) xt[j] = x[j] + alpha * p[j];
-    double f = oracle_objective(obj, xt, d);
+    double f = jitter(oracle_objective(obj, xt, d));
     *ft = f;
     *trials = k + 1;
     if (f <= f0 + c1 * alpha * ddir) return alpha;
@@ -475,6 +505,7 @@ void oracle_bfgs_run(int obj, int d, const double *x0, double theta,
         status = ZEUS_DOMAIN_ERROR;
         break;
       }
+      for (int i = 0; i < d; ++i) g[i] = jitter(g[i]);
       have_grad = 1;
       gnorm = sqrt(dot(g, g, d));
     }
@@ -486,8 +517,8 @@ void oracle_bfgs_run(int obj, int d, const double *x0, double theta,
       status = ZEUS_DIVERGED;
       break;
     }
-    for (int i = 0; i < d; ++i) p[i] = -dot(H + (size_t)i * d, g, d);
-    double f0 = oracle_objective(obj, x, d);
+    for (int i = 0; i < d; ++i) p[i] = jitter(-dot(H + (size_t)i * d, g, d));
+    double f0 = jitter(oracle_objective(obj, x, d));
     double ft;
     int trials;
     oracle_armijo(obj, d, x, p, g, f0, c1, alpha0, iter_ls, shrink, xn, &ft,
@@ -498,11 +529,14 @@ void oracle_bfgs_run(int obj, int d, const double *x0, double theta,
       status = ZEUS_DOMAIN_ERROR;
       break;
     }
+    for (int i = 0; i < d; ++i) gn[i] = jitter(gn[i]);
     for (int i = 0; i < d; ++i) {
       dx[i] = xn[i] - x[i];
       dg[i] = gn[i] - g[i];
     }
-    oracle_hessian_update(d, H, dx, dg);
+    if (oracle_hessian_update(d, H, dx, dg) && jit_state)
+      for (int i = 0; i < d; ++i)
+        for (int j = i; j < d; ++j) H[i * d + j] = H[j * d + i] = jitter(H[i * d + j]);
     memcpy(x, xn, bytes);
     memcpy(g, gn, bytes);
     gnorm = sqrt(dot(g, g, d));
@@ -531,6 +565,7 @@ typedef struct {
   double *x_final;  /* [n][d] */
   zeus_oracle_outcome *out;
   int64_t next;
+  uint64_t jitter_seed; /* 0: exact restatement */
   pthread_mutex_t lock;
 } batch_ctx;
 
@@ -543,11 +578,15 @@ static void *batch_worker(void *arg) {
     c->next = hi;
     pthread_mutex_unlock(&c->lock);
     if (lo >= c->n) break;
-    for (int64_t i = lo; i < hi; ++i)
+    for (int64_t i = lo; i < hi; ++i) {
+      uint64_t js = c->jitter_seed ^ ((uint64_t)i * 0xd1342543de82ef95ull);
+      jit_state = c->jitter_seed ? (splitmix64(&js) | 1u) : 0u;
       oracle_bfgs_run(c->obj, c->d, c->x0 + i * c->d, c->theta, c->iter_bfgs,
                       c->c1, c->alpha0, c->iter_ls, c->shrink, NULL,
                       c->out + i, c->x_final + i * c->d);
+    }
   }
+  jit_state = 0;
   return NULL;
 }
 
@@ -555,7 +594,16 @@ void oracle_bfgs_batch(int obj, int d, int64_t n, const double *x0,
                        double theta, int iter_bfgs, double c1, double alpha0,
                        int iter_ls, double shrink, int threads,
                        zeus_oracle_outcome *out, double *x_final) {
+  oracle_bfgs_batch_jitter(obj, d, n, x0, theta, iter_bfgs, c1, alpha0, iter_ls, shrink,
+                           threads, 0, out, x_final);
+}
+
+void oracle_bfgs_batch_jitter(int obj, int d, int64_t n, const double *x0,
+                              double theta, int iter_bfgs, double c1, double alpha0,
+                              int iter_ls, double shrink, int threads, uint64_t jitter_seed,
+                              zeus_oracle_outcome *out, double *x_final) {
   batch_ctx c;
+  c.jitter_seed = jitter_seed;
   c.obj = obj; c.d = d; c.iter_bfgs = iter_bfgs; c.iter_ls = iter_ls;
   c.theta = theta; c.c1 = c1; c.alpha0 = alpha0; c.shrink = shrink;
   c.n = n; c.x0 = x0; c.x_final = x_final; c.out = out; c.next = 0;

@@ -54,6 +54,11 @@ void oracle_bfgs_run(int obj, int d, const double *x0, double theta, int iter_bf
 void oracle_bfgs_batch(int obj, int d, int64_t n, const double *x0, double theta,
                        int iter_bfgs, double c1, double alpha0, int iter_ls, double shrink,
                        int threads, zeus_oracle_outcome *out, double *x_final);
+/* the batch with the rounding-jitter model (zeus_oracle.c; seed 0 = exact) */
+void oracle_bfgs_batch_jitter(int obj, int d, int64_t n, const double *x0, double theta,
+                              int iter_bfgs, double c1, double alpha0, int iter_ls,
+                              double shrink, int threads, uint64_t jitter_seed,
+                              zeus_oracle_outcome *out, double *x_final);
 int64_t oracle_reduce_best(const zeus_oracle_outcome *out, int64_t n);
 int64_t oracle_zeus_run(int obj, int d, int64_t n, uint64_t seed, double lower, double upper,
                         int iter_pso, double w, double c1_pso, double c2_pso, double theta,

@@ -14,10 +14,12 @@
 // Ownership: lane l of warp w owns coordinates c0 = 64 w + l and c1 = c0 + 32
 // (if < d): their x, p, g entries live in REGISTERS, and so do the first RR
 // rows of the two inverse-Hessian columns H[:, c0], H[:, c1]; rows RR..d-1 of
-// those columns live in the start's shared-memory slice (conflict-free: lanes
-// read consecutive columns).  The per-row broadcast values of the fused H
-// pass {g'_i, dx_i, u_i} (three [64 W] arrays, read two rows per 16-byte
-// load) are the only other shared-memory traffic.
+// those columns live either in TENSOR MEMORY (W = 1 at d = 50, Rosenbrock and
+// Rastrigin: tmem.cuh; each thread's rows in its own TMEM lane, 4-warp CTAs,
+// 3 per SM, 128 columns each) or in the start's shared-memory slice
+// (conflict-free: lanes read consecutive columns).  The per-row broadcast
+// values of the fused H pass {g'_i, dx_i, u_i} (three [64 W] arrays, read two
+// rows per 16-byte load) are the only other shared-memory traffic.
 //
 // Per iteration (reference order, bfgs.py:108-156):
 //  1. Armijo search (linesearch.py:60-71) in chunks of CH trials
@@ -40,12 +42,22 @@
 // Objective folds for d > 16 are trees: f agrees with
 // the reference's sequential fold to ~1 ulp, inside the stated tolerance.
 #include "bfgs_common.cuh"
+#include "tmem.cuh"
 
 namespace zeus {
 
 namespace {
 
 constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
+#ifndef ZEUS_WIDE_TM_WARPS
+#define ZEUS_WIDE_TM_WARPS 4
+#endif
+// TMEM kernel: CTAs of kTmWarps warps (one start each); 4 warps: 3 CTAs per
+// SM, 128 TMEM columns each; 12 warps: one CTA per SM owning all 512 columns
+constexpr int kTmWarps = ZEUS_WIDE_TM_WARPS;
+constexpr int kTmAlloc = kTmWarps == 4 ? 128 : 512;   // columns allocated per CTA
+constexpr int kTmCols = kTmWarps == 4 ? 128 : 168;    // columns per warp (lane quarter share)
+constexpr int kTmCtas = kTmWarps == 4 ? 3 : 1;        // CTAs per SM
 
 // Term j's coordinate accessor: x(j) -> xj, x(j + 1) -> xj1 (Rosenbrock's
 // neighbour); objectives only ever ask for these two.
@@ -94,6 +106,15 @@ struct WideShape {
   static constexpr int MINB = W > 1 ? 4 : 6;
 #endif
   static constexpr int CH = Obj::kId == ZEUS_OBJ_ACKLEY ? 1 : 2;
+  // TMEM layout (W = 1): rows RR_TM.. of the two columns in Tensor Memory,
+  // the first RR_TM rows in registers.  One CTA of 12 warps per SM owns all
+  // 512 TMEM columns; the 3 warps sharing a lane quarter get 168 columns
+  // (84 doubles = 42 rows of two columns) each.
+#ifdef ZEUS_WIDE_RR_TM
+  static constexpr int RR_TM = ZEUS_WIDE_RR_TM;
+#else
+  static constexpr int RR_TM = ZEUS_WIDE_TM_WARPS == 4 ? 18 : 8;
+#endif
 #ifdef ZEUS_WIDE_SMEM_STEP
   static constexpr int SR = ZEUS_WIDE_SMEM_STEP;
 #else
@@ -111,10 +132,19 @@ __host__ __device__ inline int wide_slot_doubles(int d, int rr, int w) {
 
 // D > 0: the kernel compiled for that dimension (row loops fully unrolled,
 // shared-memory offsets immediate); D = 0: any 32 < d <= 64 W at run time.
-template <class Obj, int RR, int W, int D>
+template <class Obj, int RR, int W, int D, bool TM = false>
 struct WideStart {
   static constexpr int NA = Obj::NACC;
   static constexpr int LD = 64 * W;  // row stride of the shared-memory H rows
+  // TM: rows RR.. in Tensor Memory (4 columns per row: H[i][c0], H[i][c1])
+  static constexpr int NTR = TM ? D - RR : 0;
+#ifndef ZEUS_WIDE_TMR
+#define ZEUS_WIDE_TMR 4
+#endif
+  static constexpr int TR = ZEUS_WIDE_TMR;  // rows per TMEM access (4 TR columns)
+  static_assert(!TM || (W == 1 && NTR > 0 && NTR % TR == 0 && 4 * NTR <= kTmCols),
+                "TMEM rows: W = 1, whole accesses, <= kTmCols columns per warp");
+  uint32_t tm = 0;     // TM: this thread's TMEM column base (lane = its thread)
   double* Hs;          // [d - RR][LD] rows RR.. of every column of the start
   double* rowv;        // [4][64 W]: g' | dx_prev | u_prev | (unused)
   double* xch;         // W > 1: [2][W][8] reductions, then xb[W], pb[W], tb[W]
@@ -337,9 +367,16 @@ struct WideStart {
       h0[i] = i == c0 ? 1.0 : 0.0;
       h1[i] = i == c1 ? 1.0 : 0.0;
     }
-    for (int i = RR; i < d; ++i) {
-      Hs[(i - RR) * LD + c0] = i == c0 ? 1.0 : 0.0;
-      Hs[(i - RR) * LD + c1] = i == c1 ? 1.0 : 0.0;
+    if constexpr (TM) {
+#pragma unroll
+      for (int i = RR; i < D; i += 2)
+        tmem::st4d(tm + 4 * (i - RR), i == c0 ? 1.0 : 0.0, i == c1 ? 1.0 : 0.0,
+                   i + 1 == c0 ? 1.0 : 0.0, i + 1 == c1 ? 1.0 : 0.0);
+    } else {
+      for (int i = RR; i < d; ++i) {
+        Hs[(i - RR) * LD + c0] = i == c0 ? 1.0 : 0.0;
+        Hs[(i - RR) * LD + c1] = i == c1 ? 1.0 : 0.0;
+      }
     }
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -509,49 +546,88 @@ struct WideStart {
           wa[(i + 1) & 3] = fma(h0[i + 1], g2.y, wa[(i + 1) & 3]);
           wb[(i + 1) & 3] = fma(h1[i + 1], g2.y, wb[(i + 1) & 3]);
         }
-        // rows RR.. from shared memory, SR per step with every load issued
-        // before the arithmetic (the loads' latency overlaps)
-        constexpr int SR = WideShape<Obj, W>::SR;  // shared-memory rows per step
-        static_assert(SR == 2 || SR == 4, "rows in pairs, four accumulators per column");
-        int i = RR;
+        if constexpr (TM) {
+          // rows RR.. from Tensor Memory: chunk ch + 1 is loaded while chunk
+          // ch is updated, used and stored back
+          tmem::wait_st();  // the previous pass's stores (long since done)
+          for (int ch = 0; ch < NTR / TR; ++ch) {
+            const int i = RR + TR * ch;
+            double gr[TR], xr[TR], ur[TR], pa[TR], pb[TR];
 #pragma unroll
-        for (; i + SR - 1 < (D > 0 ? D : d); i += SR) {
-          double2 g2[SR / 2], x2[SR / 2], u2[SR / 2];
-          double e0[SR], e1[SR];
-          double* hr = Hs + (i - RR) * LD;
+            for (int r = 0; r < TR; ++r) {
+              gr[r] = G[i + r];
+              xr[r] = DX[i + r];
+              ur[r] = U[i + r];
+              pa[r] = wa[(i + r - RR) & 3];
+              pb[r] = wb[(i + r - RR) & 3];
+            }
+            const uint32_t ta = tm + 4 * TR * ch;
+            {  // one .x2 access per double: no register shuffling
+              tmem::D2 e[2 * TR];
 #pragma unroll
-          for (int r = 0; r < SR / 2; ++r) {
-            g2[r] = *reinterpret_cast<const double2*>(G + i + 2 * r);
-            x2[r] = *reinterpret_cast<const double2*>(DX + i + 2 * r);
-            u2[r] = *reinterpret_cast<const double2*>(U + i + 2 * r);
+              for (int q = 0; q < 2 * TR; ++q) tmem::ld2(ta + 2 * q, e[q]);
+              tmem::wait_ld_n(e);
+#pragma unroll
+              for (int r = 0; r < TR; ++r) {
+                const double e0 = fma(xr[r], a0, fma(ur[r], b0, e[2 * r].v()));
+                const double e1 = fma(xr[r], a1, fma(ur[r], b1, e[2 * r + 1].v()));
+                tmem::st2(ta + 4 * r, e0);
+                tmem::st2(ta + 4 * r + 2, e1);
+                pa[r] = fma(e0, gr[r], pa[r]);
+                pb[r] = fma(e1, gr[r], pb[r]);
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < TR; ++r) {
+              wa[(i + r - RR) & 3] = pa[r];
+              wb[(i + r - RR) & 3] = pb[r];
+            }
           }
-#pragma unroll
-          for (int r = 0; r < SR; ++r) {
-            e0[r] = hr[r * LD + c0];
-            e1[r] = hr[r * LD + c1];
+        } else {
+          // rows RR.. from shared memory, SR per step with every load issued
+          // before the arithmetic (the loads' latency overlaps)
+          constexpr int SR = WideShape<Obj, W>::SR;  // shared-memory rows per step
+          static_assert(SR == 2 || SR == 4, "rows in pairs, four accumulators per column");
+          int i = RR;
+  #pragma unroll
+          for (; i + SR - 1 < (D > 0 ? D : d); i += SR) {
+            double2 g2[SR / 2], x2[SR / 2], u2[SR / 2];
+            double e0[SR], e1[SR];
+            double* hr = Hs + (i - RR) * LD;
+  #pragma unroll
+            for (int r = 0; r < SR / 2; ++r) {
+              g2[r] = *reinterpret_cast<const double2*>(G + i + 2 * r);
+              x2[r] = *reinterpret_cast<const double2*>(DX + i + 2 * r);
+              u2[r] = *reinterpret_cast<const double2*>(U + i + 2 * r);
+            }
+  #pragma unroll
+            for (int r = 0; r < SR; ++r) {
+              e0[r] = hr[r * LD + c0];
+              e1[r] = hr[r * LD + c1];
+            }
+  #pragma unroll
+            for (int r = 0; r < SR; ++r) {
+              const double xr = (r & 1) ? x2[r / 2].y : x2[r / 2].x;
+              const double ur = (r & 1) ? u2[r / 2].y : u2[r / 2].x;
+              const double gr = (r & 1) ? g2[r / 2].y : g2[r / 2].x;
+              e0[r] = fma(xr, a0, fma(ur, b0, e0[r]));
+              e1[r] = fma(xr, a1, fma(ur, b1, e1[r]));
+              hr[r * LD + c0] = e0[r];
+              hr[r * LD + c1] = e1[r];
+              wa[r] = fma(e0[r], gr, wa[r]);
+              wb[r] = fma(e1[r], gr, wb[r]);
+            }
           }
-#pragma unroll
-          for (int r = 0; r < SR; ++r) {
-            const double xr = (r & 1) ? x2[r / 2].y : x2[r / 2].x;
-            const double ur = (r & 1) ? u2[r / 2].y : u2[r / 2].x;
-            const double gr = (r & 1) ? g2[r / 2].y : g2[r / 2].x;
-            e0[r] = fma(xr, a0, fma(ur, b0, e0[r]));
-            e1[r] = fma(xr, a1, fma(ur, b1, e1[r]));
-            hr[r * LD + c0] = e0[r];
-            hr[r * LD + c1] = e1[r];
-            wa[r] = fma(e0[r], gr, wa[r]);
-            wb[r] = fma(e1[r], gr, wb[r]);
+  #pragma unroll 1
+          for (; i < (D > 0 ? D : d); ++i) {  // (the < SR remainder rows)
+            double* hr = Hs + (i - RR) * LD;
+            const double e0 = fma(DX[i], a0, fma(U[i], b0, hr[c0]));
+            const double e1 = fma(DX[i], a1, fma(U[i], b1, hr[c1]));
+            hr[c0] = e0;
+            hr[c1] = e1;
+            wa[0] = fma(e0, G[i], wa[0]);
+            wb[0] = fma(e1, G[i], wb[0]);
           }
-        }
-#pragma unroll 1
-        for (; i < (D > 0 ? D : d); ++i) {  // (the < SR remainder rows)
-          double* hr = Hs + (i - RR) * LD;
-          const double e0 = fma(DX[i], a0, fma(U[i], b0, hr[c0]));
-          const double e1 = fma(DX[i], a1, fma(U[i], b1, hr[c1]));
-          hr[c0] = e0;
-          hr[c1] = e1;
-          wa[0] = fma(e0, G[i], wa[0]);
-          wb[0] = fma(e1, G[i], wb[0]);
         }
         w0 = (wa[0] + wa[1]) + (wa[2] + wa[3]);
         w1 = (wb[0] + wb[1]) + (wb[2] + wb[3]);
@@ -649,12 +725,13 @@ struct WideStart {
   }
 };
 
-template <class Obj, int RR, int W, int D>
-__global__ void __launch_bounds__(kWideThreads, WideShape<Obj, W>::MINB)
+template <class Obj, int RR, int W, int D, bool TM>
+__global__ void __launch_bounds__(TM ? 32 * kTmWarps : kWideThreads, TM ? kTmCtas : WideShape<Obj, W>::MINB)
     bfgs_wide_kernel(BfgsArgs A) {
   extern __shared__ double sm[];
   const int l = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double* alpha_tab = sm;
+  __shared__ uint32_t tm_slot;
   if (threadIdx.x == 0) {
     double a = A.alpha0;  // alpha0 * shrink^t by repeated multiplication (linesearch.py:70)
     for (int t = 0; t < A.nalpha; ++t) {
@@ -662,14 +739,23 @@ __global__ void __launch_bounds__(kWideThreads, WideShape<Obj, W>::MINB)
       a *= A.shrink;
     }
   }
+  if constexpr (TM) {
+    if (wib == 0) tmem::alloc(&tm_slot, kTmAlloc);
+    tmem::fence_before_sync();
+  }
   __syncthreads();
-  WideStart<Obj, RR, W, D> S;
-  const int start_slot = wib / W;  // W = 1: two independent starts per block
+  WideStart<Obj, RR, W, D, TM> S;
+  if constexpr (TM) {
+    tmem::fence_after_sync();
+    // this warp's lane quarter and column range
+    S.tm = tm_slot + ((uint32_t)(wib & 3) * 32u << 16) + (uint32_t)(wib >> 2) * kTmCols;
+  }
+  const int start_slot = wib / W;  // W = 1: independent starts per block
   S.wi = wib % W;
   S.atab = alpha_tab;
   S.rowv = sm + A.nalpha + (size_t)start_slot * A.warp_doubles;
   S.Hs = S.rowv + 4 * 64 * W;
-  S.xch = S.Hs + (size_t)(A.d > RR ? A.d - RR : 0) * 64 * W;
+  S.xch = S.Hs + (size_t)(A.d > RR && !TM ? A.d - RR : 0) * 64 * W;
   __shared__ long long next;
   for (;;) {
     long long s = 0;
@@ -685,32 +771,43 @@ __global__ void __launch_bounds__(kWideThreads, WideShape<Obj, W>::MINB)
     if (s >= A.n) break;
     S.run(A, s, l);
   }
+  if constexpr (TM) {
+    tmem::wait_st();
+    tmem::fence_before_sync();
+    __syncthreads();
+    if (wib == 0) tmem::dealloc(tm_slot, kTmAlloc);
+  }
 }
 
 namespace {
 
-template <class Obj, int RR, int W, int D>
+template <class Obj, int RR, int W, int D, bool TM = false>
 int launch_wide(BfgsArgs A, cudaStream_t s) {
   A.nalpha = kAlphaTable;
-  A.warp_doubles = wide_slot_doubles(A.d, RR, W);  // per start
-  const int starts_per_block = 2 / W;
+  const int threads = TM ? 32 * kTmWarps : kWideThreads;
+  // per start: rowv only (TM: the H rows are in Tensor Memory), else the full slice
+  A.warp_doubles = TM ? 4 * 64 : wide_slot_doubles(A.d, RR, W);
+  const int starts_per_block = threads / 32 / W;
   const size_t smem =
       sizeof(double) * ((size_t)A.nalpha + (size_t)starts_per_block * A.warp_doubles);
-  auto kern = bfgs_wide_kernel<Obj, RR, W, D>;
+  auto kern = bfgs_wide_kernel<Obj, RR, W, D, TM>;
   int rc = check_cuda(
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
       "cudaFuncSetAttribute(wide)");
   if (rc) return rc;
   int per_sm = 0;
-  rc = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWideThreads, smem),
+  rc = check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem),
                   "occupancy(wide)");
   if (rc) return rc;
+  // TM: the CTAs per SM whose TMEM allocations fit the SM's 512 columns (the
+  // occupancy API reports 1 for kernels that allocate TMEM)
+  if (TM) per_sm = kTmCtas;
   const int sms = current_sm_count();
   if (per_sm < 1 || sms < 1) return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs wide: does not fit");
   int64_t grid = (int64_t)per_sm * sms;
   const int64_t need = (A.n + starts_per_block - 1) / starts_per_block;
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, kWideThreads, smem, s>>>(A);
+  kern<<<(unsigned)grid, threads, smem, s>>>(A);
   return check_launch("bfgs_wide_kernel");
 }
 
@@ -728,6 +825,15 @@ struct WideLaunch {
     } else {
       // the BASELINE dimensions get kernels compiled for them (T50: d = 50;
       // config 4: d = 100); any other 32 < d <= 128 runs the generic build
+      // d = 50: Rosenbrock / Rastrigin keep the H rows beyond the register
+      // rows in Tensor Memory (SM-cycles per start-iteration, TMEM / shared
+      // memory: Rosenbrock 556 / 628, Rastrigin 1,226 / 1,251); Ackley's
+      // two-accumulator line search needs the registers the TMEM access
+      // pattern takes (1,452 / 1,342), so it keeps the shared-memory rows
+#ifndef ZEUS_WIDE_NO_TMEM
+      if constexpr (Obj::kId != ZEUS_OBJ_ACKLEY)
+        if (A.d == 50) return launch_wide<Obj, WideShape<Obj, 1>::RR_TM, 1, 50, true>(A, s);
+#endif
       if (A.d == 50) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 50>(A, s);
       if (A.d <= 64) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 0>(A, s);
       if (A.d == 100) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2, 100>(A, s);

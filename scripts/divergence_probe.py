@@ -50,7 +50,8 @@ def main():
               f"| device k={full_d[3]} f={full_d[1]!r} status {full_d[4]}")
         prev_t = 0
         prev_to = 0
-        for j in range(0, min(cap, max(full_o.iterations[0], full_d[3])) + 1):
+        maxj = int(os.environ.get("MAXJ", cap))
+        for j in range(0, min(maxj, cap, max(full_o.iterations[0], full_d[3])) + 1):
             o = O.bfgs_batch(name, x0[None], iter_bfgs=j)
             dv = dev_run(name, x0, j)
             rel = np.max(np.abs(dv[0] - o.x_final[0])) / max(1e-300, np.max(np.abs(o.x_final[0])))

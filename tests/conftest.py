@@ -167,32 +167,52 @@ def perturbed_starts(x0, k, seed=0):
     return np.where(steps > 0, up, np.where(steps < 0, dn, x0))
 
 
-def certify(oracle, name, x0, cap, dev_status, dev_x, k=64):
+def certify(oracle, name, x0, cap, dev_status, dev_x, k=64, dev_gn=None):
     """Rounding-level certificate for a start on which two implementations
-    disagree: run the ORACLE from k starts within 1 ulp of x0.  Returns
-    'reached' when one of those runs ends with the device's status at the
-    device's minimiser (|dx| <= 1e-6), 'unstable' when the oracle's own
-    outcome changes under the perturbations (status or |dx| > 1e-6), else
-    None -- a disagreement no rounding-level change of the start explains."""
-    r = oracle.bfgs_batch(name, perturbed_starts(np.asarray(x0, dtype=np.float64), k),
-                          iter_bfgs=cap)
-    dx_dev = np.max(xdiff(r.x_final, np.asarray(dev_x)[None, :]), axis=1)
-    if np.any((r.status == dev_status) & (dx_dev <= 1e-6)):
-        return "reached"
-    base = oracle.bfgs_batch(name, np.asarray(x0, dtype=np.float64)[None, :], iter_bfgs=cap)
-    dx_base = np.max(xdiff(r.x_final, base.x_final), axis=1)
-    if np.any((r.status != base.status[0]) | (dx_base > 1e-6)):
-        return "unstable"
+    disagree.  The oracle is run from the same start under two models of
+    rounding freedom: k starts within 1 ulp of x0, and k runs of the
+    rounding-jitter model (every objective value and gradient component moved
+    by -1/0/+1 ulp, oracle.bfgs_batch(jitter_seed=...) -- the device computes
+    each of them within ~1 ulp of the reference).  Returns 'reached' when one
+    of those runs ends with the device's status at the device's minimiser
+    (|dx| <= 1e-6), 'unstable' when the oracle's own outcome changes under the
+    perturbations (status or |dx| > 1e-6), 'stall' when the disagreement is
+    only whether |g| crossed theta at the noise floor of one minimiser (both
+    sides within 1e-6 of each other, both |g| < 10 theta: one side stalled
+    there -- the Armijo test cannot resolve f below its rounding noise, so x
+    freezes at |g| ~ theta until the cap), else None -- a disagreement no
+    rounding-level change explains."""
+    x0 = np.asarray(x0, dtype=np.float64)
+    base = oracle.bfgs_batch(name, x0[None, :], iter_bfgs=cap)
+    runs = [oracle.bfgs_batch(name, perturbed_starts(x0, k), iter_bfgs=cap),
+            oracle.bfgs_batch(name, np.repeat(x0[None, :], k, axis=0), iter_bfgs=cap,
+                              jitter_seed=0x5EED)]
+    for r in runs:
+        dx_dev = np.max(xdiff(r.x_final, np.asarray(dev_x)[None, :]), axis=1)
+        if np.any((r.status == dev_status) & (dx_dev <= 1e-6)):
+            return "reached"
+    for r in runs:
+        dx_base = np.max(xdiff(r.x_final, base.x_final), axis=1)
+        if np.any((r.status != base.status[0]) | (dx_base > 1e-6)):
+            return "unstable"
+    if dev_gn is not None:
+        theta = 1e-6
+        same_point = float(np.max(xdiff(base.x_final[0], np.asarray(dev_x)))) <= 1e-6
+        if same_point and max(float(dev_gn), float(base.grad_norm[0])) < 10 * theta:
+            return "stall"
     return None
 
 
-def gate(label, dev, ref, floor_count, cert=None):
+def gate(label, dev, ref, floor_count, cert=None, ref_unstable=None):
     """The full-size parity bar (tests/test_gpu_parity_fullsize.py):
     agreeing starts within the stated tolerance; every status flip a start
     stalled near theta on both sides; the number of disagreements (flips +
     different minima) at most 2 x the oracle-vs-reference noise floor + 2;
     and, with ``cert = (oracle, name, starts, cap)``, every disagreement
-    certified at the rounding level (certify())."""
+    certified at the rounding level (certify()); with ``ref_unstable`` (per
+    start: the REFERENCE's own outcome changes when its start moves by 1 ulp,
+    measured by the golden script), every disagreement must be on such a
+    start."""
     rep = parity_report(label, dev.x_final, dev.f_final, dev.grad_norm, dev.iterations,
                         dev.status_codes, ref)
     flips, basins = disagreements(dev.status_codes, dev.x_final, dev.grad_norm,
@@ -208,15 +228,24 @@ def gate(label, dev, ref, floor_count, cert=None):
     gmax = np.maximum(dev.grad_norm[flips], np.asarray(ref.grad_norm)[flips])
     assert np.all(gmax < FLOOR_GN), (label, flips[gmax >= FLOOR_GN][:10])
     assert n_dis <= allowed, (label, n_dis, allowed)
+    if ref_unstable is not None and n_dis:
+        dis = np.concatenate([flips, basins])
+        bad = dis[~np.asarray(ref_unstable, dtype=bool)[dis]]
+        assert bad.size == 0, (label, "disagreement on a reference-stable start", bad[:10])
+        print(f"[parity] {label}: all {n_dis} disagreements on starts where the reference's "
+              f"own outcome changes under 1-ulp start perturbations")
     if cert is not None and n_dis:
         oracle, name, starts, cap = cert
         verdicts = {}
         for i in np.concatenate([flips, basins]):
-            v = certify(oracle, name, starts[i], cap, int(dev.status_codes[i]), dev.x_final[i])
+            v = certify(oracle, name, starts[i], cap, int(dev.status_codes[i]), dev.x_final[i],
+                        dev_gn=dev.grad_norm[i])
             verdicts[v] = verdicts.get(v, 0) + 1
             assert v is not None, (label, "uncertified disagreement at start", int(i))
-        print(f"[parity] {label}: rounding-level certificates {verdicts} (oracle from starts "
-              f"within 1 ulp: 'reached' = lands on the device's outcome)")
+        print(f"[parity] {label}: rounding-level certificates {verdicts} ('reached': the oracle "
+              f"from a start within 1 ulp or under 1-ulp rounding jitter lands on the device's "
+              f"outcome; 'unstable': the oracle's own outcome moves under them; 'stall': same "
+              f"minimiser, |g| < 10 theta on both sides, one side frozen at the noise floor)")
         rep["certificates"] = verdicts
     keep = np.ones(len(dev.status_codes), dtype=bool)
     keep[flips] = False

@@ -55,6 +55,41 @@ FIT = dict(scale=6000.0, theta=(50.0, 10.0, 5.0), edges=np.linspace(1200.0, 4800
            lower=(1.0, 0.0, 0.0), upper=(1000.0, 20.0, 10.0), seed=5)
 
 
+def perturbed(x0, k, seed):
+    """k copies of x0, each coordinate moved by -1, 0 or +1 ulp at random."""
+    rng = np.random.default_rng(seed)
+    x0 = np.asarray(x0, dtype=np.float64)
+    steps = rng.integers(-1, 2, size=(k, len(x0)))
+    up, dn = np.nextafter(x0, np.inf), np.nextafter(x0, -np.inf)
+    return np.where(steps > 0, up, np.where(steps < 0, dn, x0))
+
+
+def reference_unstable(zeus, f, cfg, outcomes, k=16):
+    """The reference's OWN rounding-level noise floor on these starts: for
+    every start that did not end in a domain error, run the reference's
+    bfgs_run (bfgs.py:80-156) from k starts within 1 ulp of it; the start is
+    unstable when any of those runs changes status or lands > 1e-6 away.
+    Starts are the reference's final swarm (driver.py:236-245)."""
+    from zeus.linesearch import LineSearchParams
+
+    streams = zeus.make_start_streams(cfg.seed, cfg.N, cfg.dim)
+    state = zeus.init_swarm(f, cfg.N, cfg.range, streams, dim=cfg.dim)
+    for _ in range(cfg.iter_pso):
+        zeus.update_swarm(state, f, cfg.pso, streams)
+    starts = np.asarray(state.positions, dtype=np.float64)
+    ls = cfg.ls if hasattr(cfg, "ls") else LineSearchParams()
+    unstable = np.zeros(cfg.N, dtype=bool)
+    for i, o in enumerate(outcomes):
+        if o.status == "domain_error":
+            continue
+        for xs in perturbed(starts[i], k, i):
+            r = zeus.bfgs_run(f, list(xs), cfg.theta, cfg.iter_bfgs, ls)
+            if r.status != o.status or np.max(np.abs(np.subtract(r.x_final, o.x_final))) > 1e-6:
+                unstable[i] = True
+                break
+    return starts, unstable
+
+
 def main() -> None:
     sys.path.insert(0, REF)
     import zeus
@@ -79,6 +114,19 @@ def main() -> None:
         data = fitting.generate_spectrum_data(model, FIT["theta"], FIT["edges"], rng=rng)
         fo = fitting.fit(model, data, FIT["lower"], FIT["upper"], seed=FIT["seed"])
         pr = fo.result.per_run
+        # the fit's scaled objective and default config (fitting.py:250-280)
+        objective = fitting.chi_square_objective(model, data)
+        lo, span = FIT["lower"], [u - l for l, u in zip(FIT["lower"], FIT["upper"])]
+
+        def scaled(u, objective=objective, lo=lo, span=span):
+            return objective([a + ui * s for ui, a, s in zip(u, lo, span)])
+
+        cfg = zeus.ZeusConfig(N=256, dim=3, range=(0.0, 1.0), iter_pso=10, iter_bfgs=600,
+                              iter_ls=40, theta=1e-8, seed=FIT["seed"])
+        starts, unstable = reference_unstable(zeus, scaled, cfg, pr)
+        out[f"{tag}_starts"] = starts
+        out[f"{tag}_ref_unstable"] = unstable
+        print(tag, "reference-unstable starts:", np.flatnonzero(unstable))
         out.update({f"{tag}_counts": data.counts, f"{tag}_theta": np.array(fo.theta),
                     f"{tag}_chi2": np.float64(fo.chi_square),
                     f"{tag}_x": np.array([o.x_final for o in pr]),

@@ -152,8 +152,15 @@ def test_validation(z):
         z.bfgs_run(z.rastrigin, [1.0], theta=0.0, iter_bfgs=10)
     with pytest.raises(ValueError):
         z.bfgs_run(z.rastrigin, [1.0], theta=1e-6, iter_bfgs=-1)
+    # a plain callable is traced into device source (trace.py) and runs
+    out = z.bfgs_run(lambda x: x[0] * x[0], [1.0], theta=1e-6, iter_bfgs=10)
+    assert out.status == z.CONVERGED and out.x_final == (0.0,)
+
+    def branchy(x):  # data-dependent control flow cannot be traced
+        return x[0] if x[0] > 0 else -x[0]
+
     with pytest.raises(NotImplementedError):
-        z.bfgs_run(lambda x: x[0] * x[0], [1.0], theta=1e-6, iter_bfgs=10)
+        z.bfgs_run(branchy, [1.0], theta=1e-6, iter_bfgs=10)
 
 
 def test_sqrt_free_convergence_and_guard_decisions(tmp_path):

@@ -87,7 +87,9 @@ def test_spectrum_fit_matches_reference(z, tag, traced):
           f"{fo.chi_square!r} vs {chi2_ref!r}, statuses {np.bincount(fo.result.per_run.status_codes, minlength=4)}")
     assert np.allclose(fo.theta, theta_ref, rtol=1e-6, atol=1e-6)
     assert abs(fo.chi_square - chi2_ref) <= 1e-8 * max(1.0, chi2_ref)
-    gate(f"{tag} fit (traced={traced}) vs reference", Dev(fo.result.per_run), Ref(g, tag), 0)
+    unstable = g[f"{tag}_ref_unstable"]
+    gate(f"{tag} fit (traced={traced}) vs reference", Dev(fo.result.per_run), Ref(g, tag),
+         int(unstable.sum()), ref_unstable=unstable)
 
 
 def test_untraceable_closure_raises(z):

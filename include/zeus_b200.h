@@ -205,6 +205,18 @@ int zeus_bench_dfma(int blocks, int threads, long long iters, double *sink, doub
 int zeus_count_within(int d, int64_t n, const double *x, int64_t ldx, const double *optimum,
                       double radius, unsigned long long *count, void *stream);
 
+/* ---- result hand-off: driver.py:244-265 (per_run, converged_count, best).
+ * Packs the per-start SoA outputs of zeus_bfgs into host-ready row-major
+ * tables in one kernel: fpack [n][d + 2] f64 = (x_final[0..d), f_final,
+ * grad_norm); ipack [n][4] i32 = (iterations, status, ls_trials, grad_evals)
+ * (16-byte aligned; NULL counters read as 0).  If spack is not NULL it also
+ * receives {tallies[0..4) (zeus_reduce_best's status counts), gbest[0] (the
+ * PSO global best f, NaN if gbest is NULL), best[0..nbest)} -- so one D2H of
+ * each table hands a whole run to the host. */
+int zeus_pack_results(const zeus_bfgs_out *out, int d, int64_t n, double *fpack, int32_t *ipack,
+                      const unsigned long long *tallies, const double *gbest, const double *best,
+                      int nbest, double *spack, void *stream);
+
 /* ---- cross-GPU early stop: driver.py:137-202 (_init_worker / _run_parallel's
  * shared Value('q') counter and Value('i') flag, one per pool).  Here the pool
  * is one process per GPU: rank 0 creates a stop block in its device memory and

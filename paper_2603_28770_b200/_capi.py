@@ -75,6 +75,8 @@ _SIGNATURES = {
     "zeus_bench_dfma": (_int, [_int, _int, ctypes.c_longlong, _vp,
                                ctypes.POINTER(_dbl), _vp]),
     "zeus_count_within": (_int, [_int, _i64, _vp, _i64, _vp, _dbl, _vp, _vp]),
+    "zeus_pack_results": (_int, [ctypes.POINTER(BfgsOut), _int, _i64, _vp, _vp, _vp, _vp, _vp,
+                                 _int, _vp, _vp]),
     "zeus_user_compile": (_int, [ctypes.c_char_p, _int, ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "zeus_user_compile_log": (ctypes.c_char_p, []),
     "zeus_user_free": (_int, [_vp]),

@@ -153,6 +153,28 @@ __device__ __forceinline__ void warp_sum8(double v[8]) {
   }
 }
 
+// 4 warp sums at once (transpose-reduce: 2+1+3 shuffles + 4 broadcasts
+// instead of 20 for 4 butterflies), identical in every lane.  Each total is
+// bitwise the butterfly warp_sum's: the pairing tree (xor 16, 8, 4, 2, 1) is
+// the same, only which lane carries which partial differs.
+__device__ __forceinline__ void warp_sum4(double v[4]) {
+  const int lane = threadIdx.x & 31;
+  const bool b16 = lane & 16, b8 = lane & 8;
+  double w2[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const double send = b16 ? v[q] : v[q + 2];
+    const double keep = b16 ? v[q + 2] : v[q];
+    w2[q] = keep + __shfl_xor_sync(kFull, send, 16);
+  }
+  double w1 = (b8 ? w2[1] : w2[0]) + __shfl_xor_sync(kFull, b8 ? w2[0] : w2[1], 8);
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) w1 += __shfl_xor_sync(kFull, w1, o);
+  // lane l now holds value index b8 + 2 b16
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v[q] = __shfl_sync(kFull, w1, ((q >> 1) & 1) * 16 | (q & 1) * 8);
+}
+
 // Warp sum when only lanes 0..LANES-1 hold non-zero values; all lanes get it.
 template <int LANES>
 __device__ __forceinline__ double warp_sum_n(double v) {

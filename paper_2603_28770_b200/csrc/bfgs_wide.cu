@@ -187,6 +187,26 @@ struct WideStart {
       }
     }
   }
+  // v[0..3] summed over the team (one transpose-reduce: 10 shuffles)
+  __device__ __forceinline__ void team_sum4(double v[8], int l) {
+    warp_sum4(v);
+    if constexpr (W > 1) {
+      double* r = xch + slot * 8 * W;
+      slot ^= 1;
+      if (l == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) r[wi * 8 + q] = v[q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double s = r[q];
+#pragma unroll
+        for (int w = 1; w < W; ++w) s += r[w * 8 + q];
+        v[q] = s;
+      }
+    }
+  }
   // v[0], v[1] summed over the team (butterflies: 10 shuffles instead of 17)
   __device__ __forceinline__ void team_sum2(double v[8], int l) {
     v[0] = warp_sum(v[0]);
@@ -357,8 +377,14 @@ struct WideStart {
     double acc[NA];
     double f0;
     int k = 0, status = ZEUS_DIVERGED, ls_trials = 0, grads = 0;
-    double gnorm = __longlong_as_double(0x7ff0000000000000LL);
+    // |g|^2 (+inf before the first gradient): |g| < theta <=> |g|^2 <= gsq_max,
+    // so the square root is taken once, for the output (bfgs.py:118)
+    double gsq = __longlong_as_double(0x7ff0000000000000LL);
     double ddir = 0.0;
+    // this lane's share of the next line search's g.p, reduced together with
+    // the first trial chunk's objective terms (the same tree as a separate
+    // warp sum: bitwise the same ddir, one reduction chain less per iteration)
+    double pd_part = 0.0;
     bool pending = false;
 
     // ---- H = I, x = x0, rowv = 0
@@ -412,13 +438,14 @@ struct WideStart {
       }
       p0 = -g0;  // H0 = I: -(I @ g) is exact
       p1 = -g1;
-      const double gg = team_sum(fma(g1, g1, g0 * g0), l);
-      gnorm = sqrt(gg);
-      ddir = -gg;
+      const double gpart = fma(g1, g1, g0 * g0);
+      const double gg = team_sum(gpart, l);
+      gsq = gg;
+      pd_part = -gpart;  // p = -g: sums to -gg exactly (rounding is sign-symmetric)
     }
 
     for (;;) {
-      if (gnorm < A.theta) {
+      if (gsq <= A.gsq_max) {  // |g| < theta (bfgs.py:118)
         status = ZEUS_CONVERGED;
         break;
       }
@@ -450,7 +477,16 @@ struct WideStart {
           double v[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) v[q] = q < CH * NA ? sc[q % CH][q / CH] : 0.0;
-          if constexpr (CH * NA <= 2) {
+          static_assert(CH * NA < 8, "a slot for g.p");
+          if (t0 == 0) {  // g.p rides with the first chunk (slot CH * NA)
+            v[CH * NA] = pd_part;
+            if constexpr (CH * NA + 1 <= 4) {
+              team_sum4(v, l);
+            } else {
+              team_sum8(v, l);
+            }
+            ddir = v[CH * NA];
+          } else if constexpr (CH * NA <= 2) {
             team_sum2(v, l);  // butterflies (+ the warp totals for W = 2)
           } else {
             team_sum8(v, l);  // transpose-reduce
@@ -552,12 +588,19 @@ struct WideStart {
           tmem::wait_st();  // the previous pass's stores (long since done)
           for (int ch = 0; ch < NTR / TR; ++ch) {
             const int i = RR + TR * ch;
+            static_assert(RR % 2 == 0 && TR % 2 == 0, "row values in 16-byte pairs");
             double gr[TR], xr[TR], ur[TR], pa[TR], pb[TR];
 #pragma unroll
+            for (int r = 0; r < TR; r += 2) {  // one broadcast LDS.128 per two rows
+              const double2 g2 = *reinterpret_cast<const double2*>(G + i + r);
+              const double2 x2 = *reinterpret_cast<const double2*>(DX + i + r);
+              const double2 u2 = *reinterpret_cast<const double2*>(U + i + r);
+              gr[r] = g2.x, gr[r + 1] = g2.y;
+              xr[r] = x2.x, xr[r + 1] = x2.y;
+              ur[r] = u2.x, ur[r + 1] = u2.y;
+            }
+#pragma unroll
             for (int r = 0; r < TR; ++r) {
-              gr[r] = G[i + r];
-              xr[r] = DX[i + r];
-              ur[r] = U[i + r];
               pa[r] = wa[(i + r - RR) & 3];
               pb[r] = wb[(i + r - RR) & 3];
             }
@@ -652,12 +695,13 @@ struct WideStart {
       part[7] = fma(w1, gn1, w0 * gn0);
       team_sum8(part, l);  // W > 1: its barrier also ends every read of rowv
       const double curv = part[1];
-      const double ndx = sqrt(part[2]), ndg = sqrt(part[3]);
-      pending = !(curv <= kCurvatureFloor * ndx * ndg);  // bfgs.py:69-71
+      // 1/curv issued next to the guard's straight-line form (the same
+      // decision as the reference expression, without its square roots)
+      const double rinv = 1.0 / curv;
+      pending = curvature_update_sl(curv, part[2], part[3]);  // bfgs.py:69-71
       if constexpr (W == 1) __syncwarp();  // rowv (dx/u of the previous iteration) consumed
-      double pd;
       {
-        const double rho = pending ? 1.0 / curv : 0.0;
+        const double rho = pending ? rinv : 0.0;
         const double cc = pending ? fma(rho * rho, part[4], rho) : 0.0;
         const double ug = part[5], xg = part[6];
         double q0 = -w0, q1 = -w1;
@@ -685,7 +729,7 @@ struct WideStart {
         if (!own1) q1 = 0.0;
         p0 = q0;
         p1 = q1;
-        pd = fma(gn1, q1, gn0 * q0);
+        pd_part = fma(gn1, q1, gn0 * q0);
       }
       // x, g <- x_new, g_new (bfgs.py:141-145)
       x0 = xn0;
@@ -695,8 +739,7 @@ struct WideStart {
       f0 = f_new;
 #pragma unroll
       for (int a = 0; a < NA; ++a) acc[a] = acc_new[a];
-      gnorm = sqrt(part[0]);
-      ddir = team_sum(pd, l);  // np.dot(g, p) of the next line search
+      gsq = part[0];
       ++k;
       if constexpr (W == 1) __syncwarp();
       if (A.stop_flag && team_any(*(volatile int*)A.stop_flag != 0)) {
@@ -711,7 +754,7 @@ struct WideStart {
     if (own1) o.x_final[(int64_t)c1 * o.ld_out + s] = x1;
     if (wi == 0 && l == 0) {
       o.f_final[s] = f0;
-      o.grad_norm[s] = gnorm;
+      o.grad_norm[s] = sqrt(gsq);
       o.iterations[s] = k;
       o.status[s] = (uint8_t)status;
       if (o.ls_trials) o.ls_trials[s] = ls_trials;

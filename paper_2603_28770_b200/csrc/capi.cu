@@ -196,6 +196,57 @@ __global__ void count_within_kernel(int d, int64_t n, const double* x, int64_t l
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
 }
 
+// Result hand-off (driver.py:244-265 returns per_run as a list of outcomes):
+// the per-start SoA outputs packed into two row-major host-ready tables in one
+// pass -- fpack[i][0..d) = x_final, [d] = f_final, [d + 1] = grad_norm;
+// ipack[i] = {iterations, status, ls_trials, grad_evals} -- plus the scalar
+// table spack = {tallies[4], pso best f, best[0 .. nbest)}.  A 32-start x 32-
+// column tile goes through shared memory so the SoA reads (along starts) and
+// the row writes (along columns) are both coalesced.
+constexpr int kPackTile = 32;
+__global__ void pack_results_kernel(zeus_bfgs_out o, int d, int64_t n, double* fpack,
+                                    int32_t* ipack, const unsigned long long* tallies,
+                                    const double* gbest, const double* best, int nbest,
+                                    double* spack) {
+  __shared__ double tile[kPackTile][kPackTile + 1];
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  const int cols = d + 2;
+  for (int64_t i0 = (int64_t)blockIdx.x * kPackTile; i0 < n; i0 += (int64_t)gridDim.x * kPackTile) {
+    for (int k0 = 0; k0 < cols; k0 += kPackTile) {
+      for (int r = ty; r < kPackTile; r += blockDim.y) {  // r: column, tx: start
+        const int k = k0 + r;
+        const int64_t i = i0 + tx;
+        double v = 0.0;
+        if (i < n && k < cols)
+          v = k < d ? o.x_final[(int64_t)k * o.ld_out + i] : (k == d ? o.f_final[i] : o.grad_norm[i]);
+        tile[r][tx] = v;
+      }
+      __syncthreads();
+      for (int r = ty; r < kPackTile; r += blockDim.y) {  // r: start, tx: column
+        const int64_t i = i0 + r;
+        const int k = k0 + tx;
+        if (i < n && k < cols) fpack[i * cols + k] = tile[tx][r];
+      }
+      __syncthreads();
+    }
+    const int t = ty * kPackTile + tx;
+    if (t < kPackTile && i0 + t < n) {
+      const int64_t i = i0 + t;
+      int4 q;
+      q.x = o.iterations[i];
+      q.y = (int)o.status[i];
+      q.z = o.ls_trials ? o.ls_trials[i] : 0;
+      q.w = o.grad_evals ? o.grad_evals[i] : 0;
+      reinterpret_cast<int4*>(ipack)[i] = q;
+    }
+  }
+  if (spack && blockIdx.x == 0 && ty == 0) {
+    if (tx < 4) spack[tx] = tallies ? (double)tallies[tx] : 0.0;
+    if (tx == 4) spack[4] = gbest ? gbest[0] : __longlong_as_double(0x7ff8000000000000LL);
+    for (int j = tx; j < nbest; j += kPackTile) spack[5 + j] = best[j];
+  }
+}
+
 }  // namespace zeus
 
 using namespace zeus;
@@ -289,6 +340,24 @@ int zeus_count_within(int d, int64_t n, const double* x, int64_t ldx, const doub
   count_within_kernel<<<(unsigned)(want < cap ? want : cap), B, 0, as_stream(stream)>>>(
       d, n, x, ldx, optimum, radius, count);
   return check_launch("count_within_kernel");
+}
+
+int zeus_pack_results(const zeus_bfgs_out* out, int d, int64_t n, double* fpack, int32_t* ipack,
+                      const unsigned long long* tallies, const double* gbest, const double* best,
+                      int nbest, double* spack, void* stream) {
+  if (!out || d < 1 || n < 0 || nbest < 0 || (n > 0 && (!fpack || !ipack || !out->x_final ||
+      !out->f_final || !out->grad_norm || !out->iterations || !out->status)) ||
+      (spack && nbest > 0 && !best) || (n > 0 && out->ld_out < n) ||
+      ((uintptr_t)ipack & 15) != 0)
+    return set_error(ZEUS_ERR_ARGUMENT, "zeus_pack_results: bad arguments");
+  if (n == 0 && !spack) return ZEUS_OK;
+  int sms = current_sm_count();
+  const int64_t want = (n + kPackTile - 1) / kPackTile, cap = (int64_t)(sms > 0 ? sms : 148) * 16;
+  int64_t grid = want < cap ? want : cap;
+  if (grid < 1) grid = 1;
+  pack_results_kernel<<<(unsigned)grid, dim3(kPackTile, 8), 0, as_stream(stream)>>>(
+      *out, d, n, fpack, ipack, tallies, gbest, best, nbest, spack);
+  return check_launch("pack_results_kernel");
 }
 
 // ---- cross-process early-stop block (driver.py:153-177 across GPUs) --------

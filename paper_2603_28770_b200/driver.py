@@ -353,17 +353,15 @@ def _zeus_run_devices(obj, cfg: ZeusConfig, devs, starts, within, t0) -> ZeusRes
                 best[0], best[1] = math.nan, -1.0
             c["ev"][3].record(c["stream"])
             fpack = torch.empty((n, d + 2), dtype=torch.float64, device=dev)
-            fpack[:, :d] = out.x_final[:, :n].t()
-            fpack[:, d] = out.f_final[:n]
-            fpack[:, d + 1] = out.grad_norm[:n]
             ipack = torch.empty((n, 4), dtype=torch.int32, device=dev)
-            for k, t in enumerate((out.iterations, out.status, out.ls_trials, out.grad_evals)):
-                ipack[:, k] = t[:n]
             spack = torch.empty(8, dtype=torch.float64, device=dev)
-            spack[0:4] = tallies
-            spack[4] = c["gbest"][0] if c["gbest"] is not None else math.nan
-            spack[5:7] = best
-            spack[7] = cnt[0]
+            _capi.check(L.zeus_pack_results(
+                out.c_struct(n), d, n, fpack.data_ptr(), ipack.data_ptr(), tallies.data_ptr(),
+                c["gbest"].data_ptr() if c["gbest"] is not None else None, best.data_ptr(), 2,
+                spack.data_ptr(), _device.stream_ptr(dev)), "pack_results")
+            engine.LAUNCHES[0] += 1
+            if within is not None:
+                spack[7] = cnt[0]
             c["fh"] = torch.empty(fpack.shape, dtype=torch.float64, pin_memory=True)
             c["ih"] = torch.empty(ipack.shape, dtype=torch.int32, pin_memory=True)
             c["sh"] = torch.empty(8, dtype=torch.float64, pin_memory=True)
@@ -596,12 +594,14 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
         mode = "all"  # the sequential prefix cut needs the whole table on every rank
     per = -(-N // world)
     fpack = torch.empty((per if world > 1 else n, d + 2), dtype=torch.float64, device=dev)
-    fpack[:n, :d] = out.x_final[:, :n].t()
-    fpack[:n, d] = out.f_final[:n]
-    fpack[:n, d + 1] = out.grad_norm[:n]
-    ipack = torch.zeros((fpack.shape[0], 4), dtype=torch.int32, device=dev)
-    for c, t in enumerate((out.iterations, out.status, out.ls_trials, out.grad_evals)):
-        ipack[:n, c] = t[:n]
+    ipack = torch.empty((fpack.shape[0], 4), dtype=torch.int32, device=dev)
+    # scalars in one small table: tallies[4], the PSO best f, every rank's [f, idx]
+    spack = torch.empty(5 + best_dev.numel(), dtype=torch.float64, device=dev)
+    _capi.check(L.zeus_pack_results(
+        out.c_struct(n), d, n, fpack.data_ptr(), ipack.data_ptr(), tallies.data_ptr(),
+        gbest.data_ptr() if gbest is not None else None, best_dev.data_ptr(), best_dev.numel(),
+        spack.data_ptr(), _device.stream_ptr(dev)), "pack_results")
+    engine.LAUNCHES[0] += 1
     base = lo
     if world > 1 and mode == "local":
         fpack, ipack = fpack[:n], ipack[:n]
@@ -618,12 +618,6 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
             base = 0
         else:
             fpack, ipack = fpack[:n], ipack[:n]
-    m_rows = fpack.shape[0]
-    # scalars in one small table: tallies[4], the PSO best f, every rank's [f, idx]
-    spack = torch.empty(5 + best_dev.numel(), dtype=torch.float64, device=dev)
-    spack[0:4] = tallies
-    spack[4] = gbest[0] if gbest is not None else math.nan
-    spack[5:] = best_dev
     fh = torch.empty(fpack.shape, dtype=torch.float64, pin_memory=True)
     ih = torch.empty(ipack.shape, dtype=torch.int32, pin_memory=True)
     fh.copy_(fpack, non_blocking=True)

@@ -6,6 +6,12 @@ import csv
 import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
+# several kernels: keep the first section (or the one named by $KERNEL)
+starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] or [0]
+want = __import__("os").environ.get("KERNEL")
+k0 = next((i for i in starts if want and want in rows[i][1]), starts[0])
+k1 = next((i for i in starts if i > k0), len(rows))
+rows = rows[k0:k1]
 h = rows[1]
 isrc, iex, istall = h.index("Source"), h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
 per = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
@@ -19,6 +25,8 @@ for r in rows[2:]:
         continue
     o = op[0] if not op[0].startswith("@") else op[1]
     o = o.split(".")[0]
+    if not r[iex].isdigit():
+        continue
     cnt[o] += int(r[iex] or 0)
     stall[o] += int(r[istall] or 0)
 tot = sum(cnt.values())

@@ -248,13 +248,16 @@ struct WideStart {
   // s[c][a] = (0 + t(c0)) + t(c1) (the team kernel's lane order).  Branch-free:
   // all 2 CH term evaluations are independent chains the scheduler can
   // interleave (a missing term is evaluated at 0 and masked out).
+  // W = 1 with d fixed: every lane's first term exists (c0 < 32 <= nt)
+  static constexpr bool kAllC0 = W == 1 && D > 0 && Obj::nterms(D) >= 32;
+
   template <class M, int CH>
   __device__ __forceinline__ void lane_terms(int d, int nt, int c0, const double al[CH],
                                              double x0, double x1, double p0, double p1,
                                              double nx0, double nx1, double np0, double np1,
                                              double s[CH][NA], bool& oor) const {
     const int c1 = c0 + 32;
-    const bool v0 = c0 < nt, v1 = c1 < nt;
+    const bool v0 = kAllC0 || c0 < nt, v1 = c1 < nt;
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const double xt0 = x0 + al[c] * p0, xt1 = x1 + al[c] * p1;
@@ -296,7 +299,7 @@ struct WideStart {
                                            double nx0, double nx1, double s[NA], double tA[2],
                                            double tB[2], bool& oor) const {
     const int c1 = c0 + 32;
-    const bool v0 = c0 < nt, v1 = c1 < nt;
+    const bool v0 = kAllC0 || c0 < nt, v1 = c1 < nt;
     double t0[NA], t1[NA], n0[Obj::KT], n1[Obj::KT];
     Obj::template term_tan<M>(LX{c0, x0, nx0}, c0, d, t0, n0, oor);
     Obj::template term_tan<M>(LX{c1, x1, nx1}, c1, d, t1, n1, oor);
@@ -459,16 +462,25 @@ struct WideStart {
       double alpha = 0.0, f_new = 0.0, acc_new[NA];
       int t_acc = -1;
       {
-#ifdef ZEUS_WIDE_CH
-        constexpr int CH = ZEUS_WIDE_CH;
+#ifdef ZEUS_WIDE_CH  // (variant builds; kept only where a slot for g.p remains)
+        constexpr int CH = ZEUS_WIDE_CH * NA < 8 ? ZEUS_WIDE_CH : WideShape<Obj, W>::CH;
 #else
         constexpr int CH = WideShape<Obj, W>::CH;
 #endif
         static_assert(CH * NA <= 8, "one reduction per chunk");
         for (int t0 = 0;; t0 += CH) {
           double al[CH], sc[CH][NA];
+          if (t0 == 0) {  // alpha0 shrink^c by the table's own repeated products
+            double a = A.alpha0;
 #pragma unroll
-          for (int c = 0; c < CH; ++c) al[c] = alpha_at(A, t0 + c);
+            for (int c = 0; c < CH; ++c) {
+              al[c] = a;
+              a *= A.shrink;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < CH; ++c) al[c] = alpha_at(A, t0 + c);
+          }
           bool oor = false;
           lane_terms<FastMath, CH>(d, nt, c0, al, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
           if (team_any(oor))  // some |2 pi x| > kTrigMax: CUDA libm, out of line
@@ -488,8 +500,10 @@ struct WideStart {
             ddir = v[CH * NA];
           } else if constexpr (CH * NA <= 2) {
             team_sum2(v, l);  // butterflies (+ the warp totals for W = 2)
+          } else if constexpr (CH * NA <= 4) {
+            team_sum4(v, l);  // transpose-reduce
           } else {
-            team_sum8(v, l);  // transpose-reduce
+            team_sum8(v, l);
           }
           unsigned pm = 0u;
           double fb[CH];

@@ -133,7 +133,7 @@ struct Rosenbrock {
   static constexpr bool kOorIsError = false;  // oor = trig range, not a DomainError
   static constexpr int kId = ZEUS_OBJ_ROSENBROCK;
   static constexpr int NACC = 1;
-  __host__ __device__ static int nterms(int d) { return d - 1; }
+  __host__ __device__ static constexpr int nterms(int d) { return d - 1; }
   __device__ static double init(int, int) { return 0.0; }
   template <class T>
   __device__ static T term2(T xj, T xj1) {
@@ -193,7 +193,7 @@ struct Rastrigin {
   static constexpr bool kOorIsError = false;  // oor = trig range, not a DomainError
   static constexpr int kId = ZEUS_OBJ_RASTRIGIN;
   static constexpr int NACC = 1;
-  __host__ __device__ static int nterms(int d) { return d; }
+  __host__ __device__ static constexpr int nterms(int d) { return d; }
   __device__ static double init(int, int d) { return 10.0 * d; }
   template <class M, class T>
   __device__ static T term1(T xi, bool& oor) {
@@ -227,7 +227,7 @@ struct Ackley {
   static constexpr bool kOorIsError = false;  // oor = trig range, not a DomainError
   static constexpr int kId = ZEUS_OBJ_ACKLEY;
   static constexpr int NACC = 2;  // sum_sq, sum_cos
-  __host__ __device__ static int nterms(int d) { return d; }
+  __host__ __device__ static constexpr int nterms(int d) { return d; }
   __device__ static double init(int, int) { return 0.0; }
   template <class M, class T>
   __device__ static void terms(T xi, T& sq, T& cs, bool& oor) {
@@ -277,7 +277,7 @@ struct GoldsteinPrice {
   static constexpr bool kOorIsError = false;  // oor = trig range, not a DomainError
   static constexpr int kId = ZEUS_OBJ_GOLDSTEIN_PRICE;
   static constexpr int NACC = 1;
-  __host__ __device__ static int nterms(int) { return 1; }
+  __host__ __device__ static constexpr int nterms(int) { return 1; }
   __device__ static double init(int, int) { return 0.0; }
   template <class T>
   __device__ static T eval(T x1, T x2) {

@@ -11,7 +11,9 @@
 // data path that bound the shared-memory layout.  Accesses here are .x2 (one
 // double = its own register pair): the .x16 vector forms made ptxas shuffle
 // registers into and out of the 16-register operand blocks (~200 moves per
-// BFGS iteration, measured), and a hand-written asm chunk fared worse.
+// BFGS iteration, measured), a hand-written asm chunk fared worse, and .x4
+// (one row's two columns per access) traded the 64 saved accesses for ~100
+// register moves around the 4-register operands (Rosenbrock d = 50 +2%).
 #pragma once
 #include <cstdint>
 

@@ -146,10 +146,10 @@ def main():
             if "dram__bytes_read.sum" not in m or not short.startswith("bfgs"):
                 continue
             obj = short[short.index("<") + 1:].split(",")[0].split(">")[0].strip().lower()
-            match = [p for p in probs if p["obj"] == obj]
-            if len(match) != 1:
+            dims = {p["d"] for p in probs if p["obj"] == obj}
+            if len(dims) != 1 or "nan" in m["dram__bytes_read.sum"][0]:
                 continue
-            key = f"{obj}{match[0]['d']}"
+            key = f"{obj}{dims.pop()}"
             rd = to_bytes(*m["dram__bytes_read.sum"])
             wr = to_bytes(*m["dram__bytes_write.sum"])
             e = entry["kernels"].setdefault(key, {"dram_bytes_per_launch": 0.0, "kernels": [],
@@ -157,8 +157,12 @@ def main():
             e["kernels"].append(short)
             e["dram_bytes_per_launch"] += rd + wr
             e["sources"].append(os.path.basename(fn))
-    if entry["kernels"]:
-        summ[args.config] = entry
+    if entry["kernels"]:  # merge per problem: a new capture replaces that problem's entry
+        cur = summ.get(args.config)
+        if not isinstance(cur, dict) or not isinstance(cur.get("kernels"), dict):
+            cur = {"kernels": {}}
+        cur["kernels"].update(entry["kernels"])
+        summ[args.config] = cur
     json.dump(summ, open(summ_path, "w"), indent=1)
 
 

@@ -49,6 +49,9 @@ namespace zeus {
 namespace {
 
 constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
+#ifndef ZEUS_WIDE_NO_SPLIT
+#define ZEUS_WIDE_NO_SPLIT 0
+#endif
 #ifndef ZEUS_WIDE_TM_WARPS
 #define ZEUS_WIDE_TM_WARPS 4
 #endif
@@ -82,6 +85,7 @@ struct WideTraits {
 };
 
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(kFull, v, src); }
+__device__ __forceinline__ double shfl_xor(double v, int m) { return __shfl_xor_sync(kFull, v, m); }
 
 }  // namespace
 
@@ -142,8 +146,21 @@ struct WideStart {
 #define ZEUS_WIDE_TMR 4
 #endif
   static constexpr int TR = ZEUS_WIDE_TMR;  // rows per TMEM access (4 TR columns)
+  // SPLIT (d = 50): the 14 lanes without a second coordinate would carry dead
+  // column slots (64 slots, 50 columns).  Instead lane l keeps column A = l
+  // (all 50 rows), half of column B = 32 + (l & 15) (rows 26 (l >> 4) + 0..25:
+  // the two halves of the warp split the column) and four rows of column
+  // C = 48 + (l >> 4) (rows (l & 15) + 16 t, t = 0..3): 80 elements per lane instead
+  // of 100, every warp instruction of the pass doing useful work.  Registers
+  // hold A rows 0..RR-1, B rows 0..RB-1 and the C rows; Tensor Memory the rest.
+  static constexpr bool SPLIT = TM && D == 50 && !ZEUS_WIDE_NO_SPLIT;
+  static constexpr int RB = SPLIT ? 32 - RR : 0;       // B rows in registers
+  static constexpr int NTA = SPLIT ? D - RR : 0;       // A rows in TMEM
+  static constexpr int NTB = SPLIT ? 26 - RB : 0;      // B rows in TMEM
   static_assert(!TM || (W == 1 && NTR > 0 && NTR % TR == 0 && 4 * NTR <= kTmCols),
                 "TMEM rows: W = 1, whole accesses, <= kTmCols columns per warp");
+  static_assert(!SPLIT || (RB > 0 && RB % 2 == 0 && NTA % 4 == 0 && NTB % 4 == 0 &&
+                           2 * (NTA + NTB) <= kTmCols), "split layout");
   uint32_t tm = 0;     // TM: this thread's TMEM column base (lane = its thread)
   double* Hs;          // [d - RR][LD] rows RR.. of every column of the start
   double* rowv;        // [4][64 W]: g' | dx_prev | u_prev | (unused)
@@ -314,6 +331,18 @@ struct WideStart {
     tB[1] = v1 && Obj::KT > 1 ? n1[Obj::KT - 1] : 0.0;
   }
 
+  // Cold path of lane_tan (some |2 pi x| > kTrigMax: CUDA libm), out of line
+  // so the hot loop's code stays small in the instruction cache.
+  __device__ __noinline__ void lane_tan_precise(int d, int nt, int c0, double x0, double x1,
+                                                double nx0, double nx1, double* s, double* tA,
+                                                double* tB) const {
+    double sv[NA], a[2], b[2];
+    bool oor = false;
+    lane_tan<PreciseMath>(d, nt, c0, x0, x1, nx0, nx1, sv, a, b, oor);
+    for (int q = 0; q < NA; ++q) s[q] = sv[q];
+    tA[0] = a[0], tA[1] = a[1], tB[0] = b[0], tB[1] = b[1];
+  }
+
   // Gradient components of c0, c1 from the lane's term tangents (+ the
   // neighbour's tangent of term c-1 w.r.t. x_c for Rosenbrock; across the
   // warp boundary it comes through the exchange scratch).
@@ -369,12 +398,109 @@ struct WideStart {
     }
   }
 
+  // SPLIT pass: the lazy rank-2 update of every element this lane keeps and
+  // its matvec partials -- wa (column A, the same accumulation order as the
+  // two-column pass), wb[0..1] (this lane's half of column B), wb[2..3]
+  // (its four rows of column C).  B / C coefficients come from the columns'
+  // owners (lanes l & 15 and 16 + (l >> 4) own coordinates 32 + .. as c1).
+  __device__ __forceinline__ void hpass_split(int l, double (&h0)[RR], double (&h1)[RB + 4],
+                                              double a0, double b0, double a1, double b1,
+                                              double (&wa)[4], double (&wb)[4]) const {
+    const double aB = shfl(a1, l & 15), bB = shfl(b1, l & 15);
+    const double aC = shfl(a1, 16 + (l >> 4)), bC = shfl(b1, 16 + (l >> 4));
+    const double* G = rowv;
+    const double* DX = rowv + LD;
+    const double* U = rowv + 2 * LD;
+    const int rB0 = 26 * (l >> 4), rC0 = l & 15;
+    const double* GB = G + rB0;
+    const double* XB = DX + rB0;
+    const double* UB = U + rB0;
+    double wbb[4] = {0.0, 0.0, 0.0, 0.0}, wc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < RR; i += 2) {  // A register rows (broadcast row values)
+      const double2 g2 = *reinterpret_cast<const double2*>(G + i);
+      const double2 x2 = *reinterpret_cast<const double2*>(DX + i);
+      const double2 u2 = *reinterpret_cast<const double2*>(U + i);
+      h0[i] = fma(x2.x, a0, fma(u2.x, b0, h0[i]));
+      h0[i + 1] = fma(x2.y, a0, fma(u2.y, b0, h0[i + 1]));
+      wa[i & 3] = fma(h0[i], g2.x, wa[i & 3]);
+      wa[(i + 1) & 3] = fma(h0[i + 1], g2.y, wa[(i + 1) & 3]);
+    }
+#pragma unroll
+    for (int t = 0; t < RB; t += 2) {  // B register rows (two rows per half-warp)
+      const double2 g2 = *reinterpret_cast<const double2*>(GB + t);
+      const double2 x2 = *reinterpret_cast<const double2*>(XB + t);
+      const double2 u2 = *reinterpret_cast<const double2*>(UB + t);
+      h1[t] = fma(x2.x, aB, fma(u2.x, bB, h1[t]));
+      h1[t + 1] = fma(x2.y, aB, fma(u2.y, bB, h1[t + 1]));
+      wbb[t & 3] = fma(h1[t], g2.x, wbb[t & 3]);
+      wbb[(t + 1) & 3] = fma(h1[t + 1], g2.y, wbb[(t + 1) & 3]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {  // the C rows: 16 consecutive rows per load (one wavefront)
+      const int r = rC0 + 16 * t;
+      h1[RB + t] = fma(DX[r], aC, fma(U[r], bC, h1[RB + t]));
+      wc[t & 1] = fma(h1[RB + t], G[r], wc[t & 1]);
+    }
+    // Tensor Memory rows in groups of 4 (A rows RR.., then B rows RB..): the
+    // next group's loads are issued while this one is updated and stored
+    tmem::wait_st();
+#pragma unroll
+    for (int gi = 0; gi < (NTA + NTB) / 4; ++gi) {
+      const bool isA = gi < NTA / 4;
+      const int r0 = isA ? RR + 4 * gi : RB + 4 * (gi - NTA / 4);  // row (A) / step (B)
+      const double* Gp = isA ? G + r0 : GB + r0;
+      const double* Xp = isA ? DX + r0 : XB + r0;
+      const double* Up = isA ? U + r0 : UB + r0;
+      const double ca = isA ? a0 : aB, cb = isA ? b0 : bB;
+      double gr[4], xr[4], ur[4];
+#pragma unroll
+      for (int r = 0; r < 4; r += 2) {
+        const double2 g2 = *reinterpret_cast<const double2*>(Gp + r);
+        const double2 x2 = *reinterpret_cast<const double2*>(Xp + r);
+        const double2 u2 = *reinterpret_cast<const double2*>(Up + r);
+        gr[r] = g2.x, gr[r + 1] = g2.y;
+        xr[r] = x2.x, xr[r + 1] = x2.y;
+        ur[r] = u2.x, ur[r + 1] = u2.y;
+      }
+      const uint32_t ta = tm + 8 * gi;
+      tmem::D2 e[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) tmem::ld2(ta + 2 * r, e[r]);
+      tmem::wait_ld_n(e);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double v = fma(xr[r], ca, fma(ur[r], cb, e[r].v()));
+        tmem::st2(ta + 2 * r, v);
+        if (isA) {
+          wa[(r0 + r - RR) & 3] = fma(v, gr[r], wa[(r0 + r - RR) & 3]);
+        } else {
+          wbb[(r0 + r) & 3] = fma(v, gr[r], wbb[(r0 + r) & 3]);
+        }
+      }
+    }
+    wb[0] = (wbb[0] + wbb[1]) + (wbb[2] + wbb[3]);
+    wb[1] = wc[0] + wc[1];
+  }
+  // w for this lane's coordinate c1 (lanes 0..17) from the split partials:
+  // column 32 + l is the sum of the two half-warp partials of lanes l, l ^ 16;
+  // columns 48 / 49 sum over the 16 lanes of the lower / upper half and go
+  // to their owners, lanes 16 / 17
+  __device__ __forceinline__ double split_w1(int l, const double (&wb)[4]) const {
+    const double wB = wb[0] + shfl_xor(wb[0], 16);
+    double wC = wb[1];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) wC += shfl_xor(wC, o);
+    const double wCo = shfl(wC, (l & 1) << 4);
+    return l < 16 ? wB : (l < 18 ? wCo : 0.0);
+  }
+
   __device__ void run(const BfgsArgs& A, long long s, int l) {
     const int d = D > 0 ? D : A.d;
     const int nt = Obj::nterms(d);
     const int c0 = 64 * wi + l, c1 = c0 + 32;
     const bool own0 = W == 1 || c0 < d, own1 = c1 < d;
-    double h0[RR], h1[RR];
+    double h0[RR], h1[SPLIT ? RB + 4 : RR];  // SPLIT: h1 = B rows 0..RB-1, then the C rows
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;  // pending rank-2 coefficients
     double x0 = 0.0, x1 = 0.0, p0 = 0.0, p1 = 0.0, g0 = 0.0, g1 = 0.0;
     double acc[NA];
@@ -391,12 +517,33 @@ struct WideStart {
     bool pending = false;
 
     // ---- H = I, x = x0, rowv = 0
+    if constexpr (SPLIT) {
+      const int cB = 32 + (l & 15), rB0 = 26 * (l >> 4), cC = 48 + (l >> 4), rC0 = l & 15;
+#pragma unroll
+      for (int i = 0; i < RR; ++i) h0[i] = i == c0 ? 1.0 : 0.0;
+#pragma unroll
+      for (int t = 0; t < RB; ++t) h1[t] = rB0 + t == cB ? 1.0 : 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) h1[RB + t] = rC0 + 16 * t == cC ? 1.0 : 0.0;
+      // TMEM: A rows RR.. at columns [0, 2 NTA), B rows RB.. after them
+#pragma unroll
+      for (int i = RR; i < D; i += 4)
+        tmem::st4d(tm + 2 * (i - RR), i == c0 ? 1.0 : 0.0, i + 1 == c0 ? 1.0 : 0.0,
+                   i + 2 == c0 ? 1.0 : 0.0, i + 3 == c0 ? 1.0 : 0.0);
+#pragma unroll
+      for (int t = RB; t < 26; t += 4)
+        tmem::st4d(tm + 2 * NTA + 2 * (t - RB), rB0 + t == cB ? 1.0 : 0.0,
+                   rB0 + t + 1 == cB ? 1.0 : 0.0, rB0 + t + 2 == cB ? 1.0 : 0.0,
+                   rB0 + t + 3 == cB ? 1.0 : 0.0);
+    } else {
 #pragma unroll
     for (int i = 0; i < RR; ++i) {
       h0[i] = i == c0 ? 1.0 : 0.0;
       h1[i] = i == c1 ? 1.0 : 0.0;
     }
-    if constexpr (TM) {
+    }
+    if constexpr (SPLIT) {
+    } else if constexpr (TM) {
 #pragma unroll
       for (int i = RR; i < D; i += 2)
         tmem::st4d(tm + 4 * (i - RR), i == c0 ? 1.0 : 0.0, i == c1 ? 1.0 : 0.0,
@@ -424,7 +571,7 @@ struct WideStart {
       double sv[NA], tA[2], tB[2];
       bool oor = false, err = false;
       lane_tan<FastMath>(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB, oor);
-      if (team_any(oor)) lane_tan<PreciseMath>(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB, oor);
+      if (team_any(oor)) lane_tan_precise(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB);
 #pragma unroll
       for (int a = 0; a < NA; ++a) acc[a] = Obj::init(a, d) + team_sum(sv[a], l);
       bool ferr = false;
@@ -556,8 +703,7 @@ struct WideStart {
         double sv[NA], tA[2], tB[2];
         bool oor = false, err = false;
         lane_tan<FastMath>(d, nt, c0, xn0, xn1, nxn0, nxn1, sv, tA, tB, oor);
-        if (team_any(oor))
-          lane_tan<PreciseMath>(d, nt, c0, xn0, xn1, nxn0, nxn1, sv, tA, tB, oor);
+        if (team_any(oor)) lane_tan_precise(d, nt, c0, xn0, xn1, nxn0, nxn1, sv, tA, tB);
         lane_grad(d, l, c0, tA, tB, acc_new, gn0, gn1, err);
         if (team_any(err)) {
           status = ZEUS_DOMAIN_ERROR;
@@ -582,6 +728,11 @@ struct WideStart {
         const double* U = rowv + 2 * LD;
         double wa[4] = {0.0, 0.0, 0.0, 0.0}, wb[4] = {0.0, 0.0, 0.0, 0.0};
         static_assert(RR % 2 == 0, "register rows in pairs");
+        if constexpr (SPLIT) {
+          hpass_split(l, h0, h1, a0, b0, a1, b1, wa, wb);
+          w0 = (wa[0] + wa[1]) + (wa[2] + wa[3]);
+          w1 = split_w1(l, wb);
+        } else {
 #pragma unroll
         for (int i = 0; i < RR; i += 2) {
           const double2 g2 = *reinterpret_cast<const double2*>(G + i);
@@ -688,6 +839,7 @@ struct WideStart {
         }
         w0 = (wa[0] + wa[1]) + (wa[2] + wa[3]);
         w1 = (wb[0] + wb[1]) + (wb[2] + wb[3]);
+        }
         // u = H_k dg = H_k g' - H_k g = w + p: p = -H_k g is this iteration's
         // direction (exact in exact arithmetic), so the pass needs one matvec
         u0 = w0 + p0;

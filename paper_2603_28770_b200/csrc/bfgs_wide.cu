@@ -14,10 +14,11 @@
 // Ownership: lane l of warp w owns coordinates c0 = 64 w + l and c1 = c0 + 32
 // (if < d): their x, p, g entries live in REGISTERS, and so do the first RR
 // rows of the two inverse-Hessian columns H[:, c0], H[:, c1]; rows RR..d-1 of
-// those columns live either in TENSOR MEMORY (W = 1 at d = 50, Rosenbrock and
-// Rastrigin: tmem.cuh; each thread's rows in its own TMEM lane, 4-warp CTAs,
-// 3 per SM, 128 columns each) or in the start's shared-memory slice
-// (conflict-free: lanes read consecutive columns).  The per-row broadcast
+// those columns live in the start's shared-memory slice (conflict-free: lanes
+// read consecutive columns).  At d = 50 (T50, Rosenbrock and Rastrigin) the
+// H elements are instead distributed by the SPLIT layout (WideStart) over
+// registers and TENSOR MEMORY (tmem.cuh: each thread's elements in its own
+// TMEM lane, 4-warp CTAs, 4 per SM, 128 columns each).  The per-row broadcast
 // values of the fused H pass {g'_i, dx_i, u_i} (three [64 W] arrays, read two
 // rows per 16-byte load) are the only other shared-memory traffic.
 //
@@ -49,18 +50,10 @@ namespace zeus {
 namespace {
 
 constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
-#ifndef ZEUS_WIDE_NO_SPLIT
-#define ZEUS_WIDE_NO_SPLIT 0
-#endif
-#ifndef ZEUS_WIDE_TM_WARPS
-#define ZEUS_WIDE_TM_WARPS 4
-#endif
-// TMEM kernel: CTAs of kTmWarps warps (one start each); 4 warps: 3 CTAs per
-// SM, 128 TMEM columns each; 12 warps: one CTA per SM owning all 512 columns
-constexpr int kTmWarps = ZEUS_WIDE_TM_WARPS;
-constexpr int kTmAlloc = kTmWarps == 4 ? 128 : 512;   // columns allocated per CTA
-constexpr int kTmCols = kTmWarps == 4 ? 128 : 168;    // columns per warp (lane quarter share)
-constexpr int kTmCtas = kTmWarps == 4 ? 3 : 1;        // CTAs per SM
+// TMEM kernel (d = 50): CTAs of 4 warps (one start each, warp w on TMEM lane
+// quarter w), each allocating 128 TMEM columns; WideShape::TM_CTAS per SM
+constexpr int kTmWarps = 4;
+constexpr int kTmAlloc = 128;  // columns allocated per CTA = columns per warp
 
 // Term j's coordinate accessor: x(j) -> xj, x(j + 1) -> xj1 (Rosenbrock's
 // neighbour); objectives only ever ask for these two.
@@ -110,14 +103,29 @@ struct WideShape {
   static constexpr int MINB = W > 1 ? 4 : 6;
 #endif
   static constexpr int CH = Obj::kId == ZEUS_OBJ_ACKLEY ? 1 : 2;
-  // TMEM layout (W = 1): rows RR_TM.. of the two columns in Tensor Memory,
-  // the first RR_TM rows in registers.  One CTA of 12 warps per SM owns all
-  // 512 TMEM columns; the 3 warps sharing a lane quarter get 168 columns
-  // (84 doubles = 42 rows of two columns) each.
+  // TMEM kernel (d = 50, split layout, WideStart): TM_CTAS 4-warp CTAs per
+  // SM, TM_NREG of a lane's 80 H elements in registers -- RR_TM rows of its
+  // column A, TM_NREG - 4 - RR_TM rows of its half column B, the 4 C rows --
+  // and the other 80 - TM_NREG in TMEM.  Measured at d = 50 (SM-cycles per
+  // start-iteration, CTAs / NREG / RR): Rosenbrock 508 (3 / 36 / 18), 476
+  // (4 / 16 / 6), 486 (4 / 20 / 10); Rastrigin 1,153 (3 / 36 / 18), 1,196
+  // (4 / 16 / 6), 1,087 (4 / 20 / 10).  4 CTAs = 16 warps per SM need <= 128
+  // registers per thread; the TMEM columns are then all allocated.
+  static constexpr bool kRosen = Obj::kId == ZEUS_OBJ_ROSENBROCK;
+#ifdef ZEUS_WIDE_TM_CTAS
+  static constexpr int TM_CTAS = ZEUS_WIDE_TM_CTAS;
+#else
+  static constexpr int TM_CTAS = 4;
+#endif
+#ifdef ZEUS_WIDE_SPLIT_NREG
+  static constexpr int TM_NREG = ZEUS_WIDE_SPLIT_NREG;
+#else
+  static constexpr int TM_NREG = kRosen ? 16 : 20;
+#endif
 #ifdef ZEUS_WIDE_RR_TM
   static constexpr int RR_TM = ZEUS_WIDE_RR_TM;
 #else
-  static constexpr int RR_TM = ZEUS_WIDE_TM_WARPS == 4 ? 18 : 8;
+  static constexpr int RR_TM = kRosen ? 6 : 10;
 #endif
 #ifdef ZEUS_WIDE_SMEM_STEP
   static constexpr int SR = ZEUS_WIDE_SMEM_STEP;
@@ -140,27 +148,21 @@ template <class Obj, int RR, int W, int D, bool TM = false>
 struct WideStart {
   static constexpr int NA = Obj::NACC;
   static constexpr int LD = 64 * W;  // row stride of the shared-memory H rows
-  // TM: rows RR.. in Tensor Memory (4 columns per row: H[i][c0], H[i][c1])
-  static constexpr int NTR = TM ? D - RR : 0;
-#ifndef ZEUS_WIDE_TMR
-#define ZEUS_WIDE_TMR 4
-#endif
-  static constexpr int TR = ZEUS_WIDE_TMR;  // rows per TMEM access (4 TR columns)
-  // SPLIT (d = 50): the 14 lanes without a second coordinate would carry dead
-  // column slots (64 slots, 50 columns).  Instead lane l keeps column A = l
-  // (all 50 rows), half of column B = 32 + (l & 15) (rows 26 (l >> 4) + 0..25:
-  // the two halves of the warp split the column) and four rows of column
-  // C = 48 + (l >> 4) (rows (l & 15) + 16 t, t = 0..3): 80 elements per lane instead
-  // of 100, every warp instruction of the pass doing useful work.  Registers
-  // hold A rows 0..RR-1, B rows 0..RB-1 and the C rows; Tensor Memory the rest.
-  static constexpr bool SPLIT = TM && D == 50 && !ZEUS_WIDE_NO_SPLIT;
-  static constexpr int RB = SPLIT ? 32 - RR : 0;       // B rows in registers
+  // TM (d = 50): the SPLIT layout -- the 14 lanes without a second
+  // coordinate would carry dead column slots (64 slots, 50 columns).  Lane l
+  // keeps column A = l (all 50 rows), half of column B = 32 + (l & 15) (rows
+  // 26 (l >> 4) + 0..25: the two halves of the warp split the column) and
+  // four rows of column C = 48 + (l >> 4) (rows (l & 15) + 16 t, t = 0..3):
+  // 80 elements per lane instead of 100, every warp instruction of the pass
+  // doing useful work.  Registers hold A rows 0..RR-1, B rows 0..RB-1 and the
+  // C rows; Tensor Memory the rest (A rows first, then B rows).
+  static constexpr bool SPLIT = TM;
+  static_assert(!TM || (W == 1 && D == 50), "TMEM kernel: the d = 50 split layout");
+  static constexpr int RB = SPLIT ? WideShape<Obj, 1>::TM_NREG - 4 - RR : 0;  // B rows in registers
   static constexpr int NTA = SPLIT ? D - RR : 0;       // A rows in TMEM
   static constexpr int NTB = SPLIT ? 26 - RB : 0;      // B rows in TMEM
-  static_assert(!TM || (W == 1 && NTR > 0 && NTR % TR == 0 && 4 * NTR <= kTmCols),
-                "TMEM rows: W = 1, whole accesses, <= kTmCols columns per warp");
   static_assert(!SPLIT || (RB > 0 && RB % 2 == 0 && NTA % 4 == 0 && NTB % 4 == 0 &&
-                           2 * (NTA + NTB) <= kTmCols), "split layout");
+                           2 * (NTA + NTB) <= kTmAlloc), "split layout");
   uint32_t tm = 0;     // TM: this thread's TMEM column base (lane = its thread)
   double* Hs;          // [d - RR][LD] rows RR.. of every column of the start
   double* rowv;        // [4][64 W]: g' | dx_prev | u_prev | (unused)
@@ -537,18 +539,10 @@ struct WideStart {
                    rB0 + t + 3 == cB ? 1.0 : 0.0);
     } else {
 #pragma unroll
-    for (int i = 0; i < RR; ++i) {
-      h0[i] = i == c0 ? 1.0 : 0.0;
-      h1[i] = i == c1 ? 1.0 : 0.0;
-    }
-    }
-    if constexpr (SPLIT) {
-    } else if constexpr (TM) {
-#pragma unroll
-      for (int i = RR; i < D; i += 2)
-        tmem::st4d(tm + 4 * (i - RR), i == c0 ? 1.0 : 0.0, i == c1 ? 1.0 : 0.0,
-                   i + 1 == c0 ? 1.0 : 0.0, i + 1 == c1 ? 1.0 : 0.0);
-    } else {
+      for (int i = 0; i < RR; ++i) {
+        h0[i] = i == c0 ? 1.0 : 0.0;
+        h1[i] = i == c1 ? 1.0 : 0.0;
+      }
       for (int i = RR; i < d; ++i) {
         Hs[(i - RR) * LD + c0] = i == c0 ? 1.0 : 0.0;
         Hs[(i - RR) * LD + c1] = i == c1 ? 1.0 : 0.0;
@@ -747,51 +741,7 @@ struct WideStart {
           wa[(i + 1) & 3] = fma(h0[i + 1], g2.y, wa[(i + 1) & 3]);
           wb[(i + 1) & 3] = fma(h1[i + 1], g2.y, wb[(i + 1) & 3]);
         }
-        if constexpr (TM) {
-          // rows RR.. from Tensor Memory: chunk ch + 1 is loaded while chunk
-          // ch is updated, used and stored back
-          tmem::wait_st();  // the previous pass's stores (long since done)
-          for (int ch = 0; ch < NTR / TR; ++ch) {
-            const int i = RR + TR * ch;
-            static_assert(RR % 2 == 0 && TR % 2 == 0, "row values in 16-byte pairs");
-            double gr[TR], xr[TR], ur[TR], pa[TR], pb[TR];
-#pragma unroll
-            for (int r = 0; r < TR; r += 2) {  // one broadcast LDS.128 per two rows
-              const double2 g2 = *reinterpret_cast<const double2*>(G + i + r);
-              const double2 x2 = *reinterpret_cast<const double2*>(DX + i + r);
-              const double2 u2 = *reinterpret_cast<const double2*>(U + i + r);
-              gr[r] = g2.x, gr[r + 1] = g2.y;
-              xr[r] = x2.x, xr[r + 1] = x2.y;
-              ur[r] = u2.x, ur[r + 1] = u2.y;
-            }
-#pragma unroll
-            for (int r = 0; r < TR; ++r) {
-              pa[r] = wa[(i + r - RR) & 3];
-              pb[r] = wb[(i + r - RR) & 3];
-            }
-            const uint32_t ta = tm + 4 * TR * ch;
-            {  // one .x2 access per double: no register shuffling
-              tmem::D2 e[2 * TR];
-#pragma unroll
-              for (int q = 0; q < 2 * TR; ++q) tmem::ld2(ta + 2 * q, e[q]);
-              tmem::wait_ld_n(e);
-#pragma unroll
-              for (int r = 0; r < TR; ++r) {
-                const double e0 = fma(xr[r], a0, fma(ur[r], b0, e[2 * r].v()));
-                const double e1 = fma(xr[r], a1, fma(ur[r], b1, e[2 * r + 1].v()));
-                tmem::st2(ta + 4 * r, e0);
-                tmem::st2(ta + 4 * r + 2, e1);
-                pa[r] = fma(e0, gr[r], pa[r]);
-                pb[r] = fma(e1, gr[r], pb[r]);
-              }
-            }
-#pragma unroll
-            for (int r = 0; r < TR; ++r) {
-              wa[(i + r - RR) & 3] = pa[r];
-              wb[(i + r - RR) & 3] = pb[r];
-            }
-          }
-        } else {
+        {
           // rows RR.. from shared memory, SR per step with every load issued
           // before the arithmetic (the loads' latency overlaps)
           constexpr int SR = WideShape<Obj, W>::SR;  // shared-memory rows per step
@@ -935,7 +885,8 @@ struct WideStart {
 };
 
 template <class Obj, int RR, int W, int D, bool TM>
-__global__ void __launch_bounds__(TM ? 32 * kTmWarps : kWideThreads, TM ? kTmCtas : WideShape<Obj, W>::MINB)
+__global__ void __launch_bounds__(TM ? 32 * kTmWarps : kWideThreads,
+                                  TM ? WideShape<Obj, 1>::TM_CTAS : WideShape<Obj, W>::MINB)
     bfgs_wide_kernel(BfgsArgs A) {
   extern __shared__ double sm[];
   const int l = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -956,8 +907,8 @@ __global__ void __launch_bounds__(TM ? 32 * kTmWarps : kWideThreads, TM ? kTmCta
   WideStart<Obj, RR, W, D, TM> S;
   if constexpr (TM) {
     tmem::fence_after_sync();
-    // this warp's lane quarter and column range
-    S.tm = tm_slot + ((uint32_t)(wib & 3) * 32u << 16) + (uint32_t)(wib >> 2) * kTmCols;
+    // this warp's lane quarter (TMEM address: lane << 16 | column)
+    S.tm = tm_slot + ((uint32_t)(wib & 3) * 32u << 16);
   }
   const int start_slot = wib / W;  // W = 1: independent starts per block
   S.wi = wib % W;
@@ -1010,7 +961,7 @@ int launch_wide(BfgsArgs A, cudaStream_t s) {
   if (rc) return rc;
   // TM: the CTAs per SM whose TMEM allocations fit the SM's 512 columns (the
   // occupancy API reports 1 for kernels that allocate TMEM)
-  if (TM) per_sm = kTmCtas;
+  if (TM) per_sm = WideShape<Obj, 1>::TM_CTAS;
   const int sms = current_sm_count();
   if (per_sm < 1 || sms < 1) return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs wide: does not fit");
   int64_t grid = (int64_t)per_sm * sms;

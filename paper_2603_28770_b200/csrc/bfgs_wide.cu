@@ -50,6 +50,9 @@ namespace zeus {
 namespace {
 
 constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
+#ifndef ZEUS_WIDE_LAYOUT
+#define ZEUS_WIDE_LAYOUT 1  // d = 50 H layout: 0 = split, 1 = 25 x 3 blocks (WideStart)
+#endif
 // TMEM kernel (d = 50): CTAs of 4 warps (one start each, warp w on TMEM lane
 // quarter w), each allocating 128 TMEM columns; WideShape::TM_CTAS per SM
 constexpr int kTmWarps = 4;
@@ -125,7 +128,7 @@ struct WideShape {
 #ifdef ZEUS_WIDE_RR_TM
   static constexpr int RR_TM = ZEUS_WIDE_RR_TM;
 #else
-  static constexpr int RR_TM = kRosen ? 6 : 10;
+  static constexpr int RR_TM = ZEUS_WIDE_LAYOUT == 1 ? (kRosen ? 7 : 5) : (kRosen ? 6 : 10);
 #endif
 #ifdef ZEUS_WIDE_SMEM_STEP
   static constexpr int SR = ZEUS_WIDE_SMEM_STEP;
@@ -156,11 +159,21 @@ struct WideStart {
   // 80 elements per lane instead of 100, every warp instruction of the pass
   // doing useful work.  Registers hold A rows 0..RR-1, B rows 0..RB-1 and the
   // C rows; Tensor Memory the rest (A rows first, then B rows).
-  static constexpr bool SPLIT = TM;
-  static_assert(!TM || (W == 1 && D == 50), "TMEM kernel: the d = 50 split layout");
+  static constexpr bool BLK3 = TM && ZEUS_WIDE_LAYOUT == 1;
+  static constexpr bool SPLIT = TM && !BLK3;
+  // BLK3 (d = 50): lane l = 16 q + p keeps rows 2 r + q (r = 0..24) of
+  // columns 3 p .. 3 p + 2 plus the four C rows: 79 elements; one load of a
+  // row value serves both row parities (16 contiguous bytes, one wavefront)
+  // and three columns.  Update coefficients by column in shared memory
+  // (written by the owners), column sums over the two q lanes by one
+  // shuffle, handed to the owners through the spare rowv row.
+  static constexpr int NT3 = BLK3 ? 25 - RR : 0;  // BLK3 rows in TMEM
+  static_assert(!BLK3 || (NT3 % 2 == 0 && 6 * NT3 <= kTmAlloc), "blk3 layout");
   static constexpr int RB = SPLIT ? WideShape<Obj, 1>::TM_NREG - 4 - RR : 0;  // B rows in registers
   static constexpr int NTA = SPLIT ? D - RR : 0;       // A rows in TMEM
   static constexpr int NTB = SPLIT ? 26 - RB : 0;      // B rows in TMEM
+  static constexpr int H0N = BLK3 ? 1 : RR;  // register arrays of the pass
+  static constexpr int H1N = BLK3 ? 3 * RR + 4 : (SPLIT ? RB + 4 : RR);
   static_assert(!SPLIT || (RB > 0 && RB % 2 == 0 && NTA % 4 == 0 && NTB % 4 == 0 &&
                            2 * (NTA + NTB) <= kTmAlloc), "split layout");
   uint32_t tm = 0;     // TM: this thread's TMEM column base (lane = its thread)
@@ -400,6 +413,86 @@ struct WideStart {
     }
   }
 
+  // BLK3 pass: the lazy rank-2 update of the lane's 79 elements and their
+  // matvec partials; returns w = H g' for the lane's coordinates c0, c1.
+  __device__ __forceinline__ void hpass_blk3(int l, double (&h1)[H1N], double a1, double b1,
+                                             double& w0, double& w1) const {
+    const int q = l >> 4, pq = l & 15, rC0 = l & 15;
+    const double* CF = rowv + 4 * LD + 6 * pq;  // (a, b) of columns 3 p + k
+    double a[3], b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double2 ab = *reinterpret_cast<const double2*>(CF + 2 * k);
+      a[k] = ab.x;
+      b[k] = ab.y;
+    }
+    const double aC = shfl(a1, 16 + (l >> 4)), bC = shfl(b1, 16 + (l >> 4));
+    const double* G = rowv + q;
+    const double* DX = rowv + LD + q;
+    const double* U = rowv + 2 * LD + q;
+    double w[3] = {0.0, 0.0, 0.0}, wc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {  // register rows: row 2 r + q
+      const double g = G[2 * r], x = DX[2 * r], u = U[2 * r];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        h1[3 * r + k] = fma(x, a[k], fma(u, b[k], h1[3 * r + k]));
+        w[k] = fma(h1[3 * r + k], g, w[k]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {  // the C rows: 16 consecutive rows per load
+      const int r = rC0 + 16 * t;
+      h1[3 * RR + t] = fma(rowv[LD + r], aC, fma(rowv[2 * LD + r], bC, h1[3 * RR + t]));
+      wc[t & 1] = fma(h1[3 * RR + t], rowv[r], wc[t & 1]);
+    }
+    tmem::wait_st();
+#ifndef ZEUS_WIDE_B3_NR
+#define ZEUS_WIDE_B3_NR 2
+#endif
+    constexpr int NR = ZEUS_WIDE_B3_NR;  // TMEM rows per wait (3 NR elements)
+    static_assert(NT3 % NR == 0, "whole TMEM groups");
+#pragma unroll
+    for (int r0 = RR; r0 < 25; r0 += NR) {
+      double gr[NR], xr[NR], ur[NR];
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        gr[j] = G[2 * (r0 + j)];
+        xr[j] = DX[2 * (r0 + j)];
+        ur[j] = U[2 * (r0 + j)];
+      }
+      const uint32_t ta = tm + 6 * (r0 - RR);
+      tmem::D2 e[3 * NR];
+#pragma unroll
+      for (int j = 0; j < 3 * NR; ++j) tmem::ld2(ta + 2 * j, e[j]);
+      tmem::wait_ld_n(e);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double v = fma(xr[j], a[k], fma(ur[j], b[k], e[3 * j + k].v()));
+          tmem::st2(ta + 6 * j + 2 * k, v);
+          w[k] = fma(v, gr[j], w[k]);
+        }
+      }
+    }
+    // column sums over the two row parities (lanes l, l ^ 16)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) w[k] += shfl_xor(w[k], 16);
+    double* wv = rowv + 3 * LD;  // the spare row: w by column
+    if (q == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) wv[3 * pq + k] = w[k];
+    }
+    double c = wc[0] + wc[1];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) c += shfl_xor(c, o);
+    if (rC0 == 0) wv[48 + (l >> 4)] = c;
+    __syncwarp();
+    w0 = wv[l];
+    w1 = l < 18 ? wv[32 + l] : 0.0;
+  }
+
   // SPLIT pass: the lazy rank-2 update of every element this lane keeps and
   // its matvec partials -- wa (column A, the same accumulation order as the
   // two-column pass), wb[0..1] (this lane's half of column B), wb[2..3]
@@ -502,7 +595,9 @@ struct WideStart {
     const int nt = Obj::nterms(d);
     const int c0 = 64 * wi + l, c1 = c0 + 32;
     const bool own0 = W == 1 || c0 < d, own1 = c1 < d;
-    double h0[RR], h1[SPLIT ? RB + 4 : RR];  // SPLIT: h1 = B rows 0..RB-1, then the C rows
+    // SPLIT: h0 = A rows, h1 = B rows 0..RB-1 then the C rows; BLK3: h1 = the
+    // block's register rows [RR][3] then the C rows
+    double h0[H0N], h1[H1N];
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;  // pending rank-2 coefficients
     double x0 = 0.0, x1 = 0.0, p0 = 0.0, p1 = 0.0, g0 = 0.0, g1 = 0.0;
     double acc[NA];
@@ -519,7 +614,27 @@ struct WideStart {
     bool pending = false;
 
     // ---- H = I, x = x0, rowv = 0
-    if constexpr (SPLIT) {
+    if constexpr (BLK3) {
+      const int q = l >> 4, pq = l & 15, cC = 48 + (l >> 4), rC0 = l & 15;
+#pragma unroll
+      for (int r = 0; r < 25; ++r) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double e = 2 * r + q == 3 * pq + k ? 1.0 : 0.0;
+          if (r < RR) {
+            h1[3 * r + k] = e;
+          } else {
+            tmem::st2(tm + 6 * (r - RR) + 2 * k, e);
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) h1[3 * RR + t] = rC0 + 16 * t == cC ? 1.0 : 0.0;
+      rowv[4 * LD + 2 * c0] = 0.0;  // column coefficients (a, b) by column
+      rowv[4 * LD + 2 * c0 + 1] = 0.0;
+      rowv[4 * LD + 2 * c1] = 0.0;
+      rowv[4 * LD + 2 * c1 + 1] = 0.0;
+    } else if constexpr (SPLIT) {
       const int cB = 32 + (l & 15), rB0 = 26 * (l >> 4), cC = 48 + (l >> 4), rC0 = l & 15;
 #pragma unroll
       for (int i = 0; i < RR; ++i) h0[i] = i == c0 ? 1.0 : 0.0;
@@ -721,8 +836,10 @@ struct WideStart {
         const double* DX = rowv + LD;
         const double* U = rowv + 2 * LD;
         double wa[4] = {0.0, 0.0, 0.0, 0.0}, wb[4] = {0.0, 0.0, 0.0, 0.0};
-        static_assert(RR % 2 == 0, "register rows in pairs");
-        if constexpr (SPLIT) {
+        static_assert(BLK3 || RR % 2 == 0, "register rows in pairs");
+        if constexpr (BLK3) {
+          hpass_blk3(l, h1, a1, b1, w0, w1);
+        } else if constexpr (SPLIT) {
           hpass_split(l, h0, h1, a0, b0, a1, b1, wa, wb);
           w0 = (wa[0] + wa[1]) + (wa[2] + wa[3]);
           w1 = split_w1(l, wb);
@@ -841,6 +958,10 @@ struct WideStart {
           rowv[LD + c1] = rx1;
           rowv[2 * LD + c1] = ru1;
         }
+        if constexpr (BLK3) {  // the pass reads every column's (a, b) here
+          *reinterpret_cast<double2*>(rowv + 4 * LD + 2 * c0) = make_double2(a0, b0);
+          if (own1) *reinterpret_cast<double2*>(rowv + 4 * LD + 2 * c1) = make_double2(a1, b1);
+        }
         if (!own0) q0 = 0.0;
         if (!own1) q1 = 0.0;
         p0 = q0;
@@ -946,7 +1067,7 @@ int launch_wide(BfgsArgs A, cudaStream_t s) {
   A.nalpha = kAlphaTable;
   const int threads = TM ? 32 * kTmWarps : kWideThreads;
   // per start: rowv only (TM: the H rows are in Tensor Memory), else the full slice
-  A.warp_doubles = TM ? 4 * 64 : wide_slot_doubles(A.d, RR, W);
+  A.warp_doubles = TM ? (ZEUS_WIDE_LAYOUT == 1 ? 6 : 4) * 64 : wide_slot_doubles(A.d, RR, W);
   const int starts_per_block = threads / 32 / W;
   const size_t smem =
       sizeof(double) * ((size_t)A.nalpha + (size_t)starts_per_block * A.warp_doubles);

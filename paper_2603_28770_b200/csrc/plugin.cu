@@ -307,7 +307,7 @@ int zeus_user_pso_sweep(void* handle, int64_t n, int64_t i0, uint64_t seed, int 
                         int64_t ld, const double* gX, double* cand, void* workspace,
                         void* stream) {
   UserPlugin* up = (UserPlugin*)handle;
-  if (!up || n < 1 || i0 < 0 || ld < n || sweep < 0 || !x || !v || !pbest || !pval || !gX ||
+  if (!up || n < 1 || i0 < 0 || ld < n || sweep < -1 || !x || !v || !pbest || !pval || !gX ||
       !cand || !workspace)
     return set_error(ZEUS_ERR_ARGUMENT, "zeus_user_pso_sweep: bad arguments");
   int d = up->d;

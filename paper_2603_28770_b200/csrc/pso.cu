@@ -194,7 +194,7 @@ int zeus_pso_init(int obj, int d, int64_t n, int64_t i0, uint64_t seed, double l
 int zeus_pso_sweep(int obj, int d, int64_t n, int64_t i0, uint64_t seed, int sweep, double w,
                    double c1, double c2, double* x, double* v, double* pbest, double* pval,
                    int64_t ld, const double* gX, double* cand, void* workspace, void* stream) {
-  if (d < 1 || n < 1 || i0 < 0 || ld < n || sweep < 0 || !x || !v || !pbest || !pval || !gX ||
+  if (d < 1 || n < 1 || i0 < 0 || ld < n || sweep < -1 || !x || !v || !pbest || !pval || !gX ||
       !cand || !workspace || (obj == ZEUS_OBJ_GOLDSTEIN_PRICE && d != 2))
     return set_error(ZEUS_ERR_ARGUMENT, "zeus_pso_sweep: bad arguments");
   const int rc = dispatch_objective<PsoSweepLaunch>(obj, d, n, i0, seed, sweep, w, c1, c2, x,

@@ -62,8 +62,24 @@ __device__ __forceinline__ void ld2(uint32_t a, D2& d) {
 }
 template <int N>
 __device__ __forceinline__ void wait_ld_n(D2 (&d)[N]) {
-  static_assert(N == 8 || N == 4, "wait_ld_n: 4 or 8 doubles");
-  if constexpr (N == 8)
+  static_assert(N == 12 || N == 8 || N == 6 || N == 4, "wait_ld_n: 4, 6, 8 or 12 doubles");
+  if constexpr (N == 12)
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                 : "+r"(d[0].lo), "+r"(d[0].hi), "+r"(d[1].lo), "+r"(d[1].hi), "+r"(d[2].lo),
+                   "+r"(d[2].hi), "+r"(d[3].lo), "+r"(d[3].hi), "+r"(d[4].lo), "+r"(d[4].hi),
+                   "+r"(d[5].lo), "+r"(d[5].hi), "+r"(d[6].lo), "+r"(d[6].hi), "+r"(d[7].lo),
+                   "+r"(d[7].hi), "+r"(d[8].lo), "+r"(d[8].hi), "+r"(d[9].lo), "+r"(d[9].hi),
+                   "+r"(d[10].lo), "+r"(d[10].hi), "+r"(d[11].lo), "+r"(d[11].hi)
+                 :
+                 : "memory");
+  else if constexpr (N == 6)
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                 : "+r"(d[0].lo), "+r"(d[0].hi), "+r"(d[1].lo), "+r"(d[1].hi), "+r"(d[2].lo),
+                   "+r"(d[2].hi), "+r"(d[3].lo), "+r"(d[3].hi), "+r"(d[4].lo), "+r"(d[4].hi),
+                   "+r"(d[5].lo), "+r"(d[5].hi)
+                 :
+                 : "memory");
+  else if constexpr (N == 8)
     asm volatile("tcgen05.wait::ld.sync.aligned;\n"
                  : "+r"(d[0].lo), "+r"(d[0].hi), "+r"(d[1].lo), "+r"(d[1].hi), "+r"(d[2].lo),
                    "+r"(d[2].hi), "+r"(d[3].lo), "+r"(d[3].hi), "+r"(d[4].lo), "+r"(d[4].hi),

@@ -34,7 +34,10 @@ def _evaluate(obj_id: int, x: Sequence[float]) -> float:
     import torch
 
     from . import _device
+    from .autodiff import Dual
 
+    if any(isinstance(v, Dual) for v in x):
+        return _evaluate_dual(obj_id, x)
     vals = [float(v) for v in x]
     dev = _device.require_device()
     xs = torch.tensor(vals, dtype=torch.float64, device=dev).reshape(len(vals), 1)
@@ -43,6 +46,34 @@ def _evaluate(obj_id: int, x: Sequence[float]) -> float:
                                                  out.data_ptr(), _device.stream_ptr(dev)),
                 "objective")
     return float(out.item())
+
+
+def _evaluate_dual(obj_id: int, x: Sequence) -> object:
+    """The objective on Dual numbers (the reference's functions are generic
+    over float / Dual, objectives.py:33-113): the real part is the float
+    evaluation (bit for bit, as in the reference), the dual part the
+    directional derivative grad f . t from the device's forward-mode gradient
+    (summed in coordinate order; the reference propagates tangents through
+    the expression instead, so it can differ in the last bits).  DomainError
+    where the reference's Dual evaluation raises (Ackley's sqrt at sum x^2 = 0,
+    autodiff.py:207-213) -- whatever the tangents."""
+    import numpy as np
+
+    from .autodiff import DomainError, Dual
+    from . import autodiff
+
+    reals = [float(v.real) if isinstance(v, Dual) else float(v) for v in x]
+    tans = [float(v.dual) if isinstance(v, Dual) else 0.0 for v in x]
+    f = _evaluate(obj_id, reals)
+    fn = {_capi.OBJ_ROSENBROCK: rosenbrock, _capi.OBJ_RASTRIGIN: rastrigin,
+          _capi.OBJ_ACKLEY: ackley, _capi.OBJ_GOLDSTEIN_PRICE: goldstein_price}[obj_id]
+    g, err = autodiff.gradients(fn, np.asarray([reals]))
+    if err[0]:
+        raise DomainError("the Dual evaluation leaves the domain (autodiff.py:207-216)")
+    dual = 0.0
+    for gi, ti in zip(g[0].tolist(), tans):
+        dual += gi * ti
+    return Dual(f, dual)
 
 
 def rosenbrock(x: Sequence[float]) -> float:

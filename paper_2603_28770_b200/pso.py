@@ -113,7 +113,7 @@ def update_swarm(
     n, dim = state.n, state.dim
     obj = objective_id(f, dim)
     off = rng.uniform_offset()
-    if off < 2 * dim or off % (2 * dim):
+    if off % (2 * dim):  # (offset 0: a swarm not made by init_swarm, fresh streams)
         raise ValueError("stream offset does not sit on a sweep boundary")
     sweep = off // (2 * dim) - 1
     dev = _device.require_device()

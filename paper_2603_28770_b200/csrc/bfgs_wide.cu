@@ -16,7 +16,7 @@
 // rows of the two inverse-Hessian columns H[:, c0], H[:, c1]; rows RR..d-1 of
 // those columns live in the start's shared-memory slice (conflict-free: lanes
 // read consecutive columns).  At d = 50 (T50, Rosenbrock and Rastrigin) the
-// H elements are instead distributed by the SPLIT layout (WideStart) over
+// H elements are instead distributed by the BLOCK layout (WideStart) over
 // registers and TENSOR MEMORY (tmem.cuh: each thread's elements in its own
 // TMEM lane, 4-warp CTAs, 4 per SM, 128 columns each).  The per-row broadcast
 // values of the fused H pass {g'_i, dx_i, u_i} (three [64 W] arrays, read two
@@ -50,9 +50,6 @@ namespace zeus {
 namespace {
 
 constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
-#ifndef ZEUS_WIDE_LAYOUT
-#define ZEUS_WIDE_LAYOUT 1  // d = 50 H layout: 0 = split, 1 = 25 x 3 blocks (WideStart)
-#endif
 // TMEM kernel (d = 50): CTAs of 4 warps (one start each, warp w on TMEM lane
 // quarter w), each allocating 128 TMEM columns; WideShape::TM_CTAS per SM
 constexpr int kTmWarps = 4;
@@ -106,29 +103,25 @@ struct WideShape {
   static constexpr int MINB = W > 1 ? 4 : 6;
 #endif
   static constexpr int CH = Obj::kId == ZEUS_OBJ_ACKLEY ? 1 : 2;
-  // TMEM kernel (d = 50, split layout, WideStart): TM_CTAS 4-warp CTAs per
-  // SM, TM_NREG of a lane's 80 H elements in registers -- RR_TM rows of its
-  // column A, TM_NREG - 4 - RR_TM rows of its half column B, the 4 C rows --
-  // and the other 80 - TM_NREG in TMEM.  Measured at d = 50 (SM-cycles per
-  // start-iteration, CTAs / NREG / RR): Rosenbrock 508 (3 / 36 / 18), 476
-  // (4 / 16 / 6), 486 (4 / 20 / 10); Rastrigin 1,153 (3 / 36 / 18), 1,196
-  // (4 / 16 / 6), 1,087 (4 / 20 / 10).  4 CTAs = 16 warps per SM need <= 128
-  // registers per thread; the TMEM columns are then all allocated.
+  // TMEM kernel (d = 50, the block layout of WideStart): TM_CTAS 4-warp CTAs
+  // per SM (4 = 16 warps: <= 128 registers per thread, all 512 TMEM columns
+  // allocated), RR_TM of a lane's 25 block rows in registers, the rest in
+  // TMEM.  Measured at d = 50 (SM-cycles per start-iteration): the split
+  // layout that preceded it (column l + half a column + 4 rows per lane,
+  // 80 elements) Rosenbrock 508 at 3 CTAs / 36 register elements, 476 at
+  // 4 / 16; Rastrigin 1,153 / 1,087; this layout Rosenbrock 448 (RR 7),
+  // 454 (5), 492 (9), 516 (11); Rastrigin 1,062 (5), 1,070 (7), 1,085 (9);
+  // 3 CTAs (168 registers, RR 9): 484 / 1,173.
   static constexpr bool kRosen = Obj::kId == ZEUS_OBJ_ROSENBROCK;
 #ifdef ZEUS_WIDE_TM_CTAS
   static constexpr int TM_CTAS = ZEUS_WIDE_TM_CTAS;
 #else
   static constexpr int TM_CTAS = 4;
 #endif
-#ifdef ZEUS_WIDE_SPLIT_NREG
-  static constexpr int TM_NREG = ZEUS_WIDE_SPLIT_NREG;
-#else
-  static constexpr int TM_NREG = kRosen ? 16 : 20;
-#endif
 #ifdef ZEUS_WIDE_RR_TM
   static constexpr int RR_TM = ZEUS_WIDE_RR_TM;
 #else
-  static constexpr int RR_TM = ZEUS_WIDE_LAYOUT == 1 ? (kRosen ? 7 : 5) : (kRosen ? 6 : 10);
+  static constexpr int RR_TM = kRosen ? 7 : 5;
 #endif
 #ifdef ZEUS_WIDE_SMEM_STEP
   static constexpr int SR = ZEUS_WIDE_SMEM_STEP;
@@ -151,34 +144,27 @@ template <class Obj, int RR, int W, int D, bool TM = false>
 struct WideStart {
   static constexpr int NA = Obj::NACC;
   static constexpr int LD = 64 * W;  // row stride of the shared-memory H rows
-  // TM (d = 50): the SPLIT layout -- the 14 lanes without a second
-  // coordinate would carry dead column slots (64 slots, 50 columns).  Lane l
-  // keeps column A = l (all 50 rows), half of column B = 32 + (l & 15) (rows
-  // 26 (l >> 4) + 0..25: the two halves of the warp split the column) and
-  // four rows of column C = 48 + (l >> 4) (rows (l & 15) + 16 t, t = 0..3):
-  // 80 elements per lane instead of 100, every warp instruction of the pass
-  // doing useful work.  Registers hold A rows 0..RR-1, B rows 0..RB-1 and the
-  // C rows; Tensor Memory the rest (A rows first, then B rows).
-  static constexpr bool BLK3 = TM && ZEUS_WIDE_LAYOUT == 1;
-  static constexpr bool SPLIT = TM && !BLK3;
-  // BLK3 (d = 50): lane l = 16 q + p keeps rows 2 r + q (r = 0..24) of
-  // columns 3 p .. 3 p + 2 plus the four C rows: 79 elements; one load of a
-  // row value serves both row parities (16 contiguous bytes, one wavefront)
-  // and three columns.  Update coefficients by column in shared memory
-  // (written by the owners), column sums over the two q lanes by one
-  // shuffle, handed to the owners through the spare rowv row.
-  static constexpr int NT3 = BLK3 ? 25 - RR : 0;  // BLK3 rows in TMEM
-  static_assert(!BLK3 || (NT3 % 2 == 0 && 6 * NT3 <= kTmAlloc), "blk3 layout");
-  static constexpr int RB = SPLIT ? WideShape<Obj, 1>::TM_NREG - 4 - RR : 0;  // B rows in registers
-  static constexpr int NTA = SPLIT ? D - RR : 0;       // A rows in TMEM
-  static constexpr int NTB = SPLIT ? 26 - RB : 0;      // B rows in TMEM
+  // TM (d = 50): the BLOCK layout.  Lane l owning columns l and l + 32
+  // would leave 14 of a warp's 64 column slots empty at d = 50, and one load
+  // of a row value would serve one or two elements per lane.  Instead lane
+  // l = 16 q + p keeps rows 2 r + q (r = 0..24) of columns 3 p .. 3 p + 2
+  // (columns 0..47) plus rows (l & 15) + 16 t (t = 0..3) of column
+  // 48 + (l >> 4): 79 elements, no dead slot, and one load of a row value
+  // (g', dx, u: 16 contiguous bytes for the two parities, one shared-memory
+  // wavefront) serves three columns.  The update coefficients of every
+  // column are in shared memory (written by the owners); the column sums
+  // are completed over the two parities by one shuffle and handed to the
+  // owners through the spare rowv row.  RR block rows in registers, the
+  // other NT3 in Tensor Memory.
+  static constexpr bool BLK3 = TM;
+  static_assert(!TM || (W == 1 && D == 50), "TMEM kernel: the d = 50 block layout");
+  static constexpr int NT3 = BLK3 ? 25 - RR : 0;  // block rows in TMEM
+  static_assert(!BLK3 || (NT3 % 2 == 0 && 6 * NT3 <= kTmAlloc), "block layout");
   static constexpr int H0N = BLK3 ? 1 : RR;  // register arrays of the pass
-  static constexpr int H1N = BLK3 ? 3 * RR + 4 : (SPLIT ? RB + 4 : RR);
-  static_assert(!SPLIT || (RB > 0 && RB % 2 == 0 && NTA % 4 == 0 && NTB % 4 == 0 &&
-                           2 * (NTA + NTB) <= kTmAlloc), "split layout");
+  static constexpr int H1N = BLK3 ? 3 * RR + 4 : RR;
   uint32_t tm = 0;     // TM: this thread's TMEM column base (lane = its thread)
   double* Hs;          // [d - RR][LD] rows RR.. of every column of the start
-  double* rowv;        // [4][64 W]: g' | dx_prev | u_prev | (unused)
+  double* rowv;        // [4][64 W]: g' | dx_prev | u_prev | w (TM); TM: + [64][2] (a, b)
   double* xch;         // W > 1: [2][W][8] reductions, then xb[W], pb[W], tb[W]
   const double* atab;  // block alpha table
   int wi = 0;          // warp index within the start (0 .. W-1)
@@ -493,110 +479,13 @@ struct WideStart {
     w1 = l < 18 ? wv[32 + l] : 0.0;
   }
 
-  // SPLIT pass: the lazy rank-2 update of every element this lane keeps and
-  // its matvec partials -- wa (column A, the same accumulation order as the
-  // two-column pass), wb[0..1] (this lane's half of column B), wb[2..3]
-  // (its four rows of column C).  B / C coefficients come from the columns'
-  // owners (lanes l & 15 and 16 + (l >> 4) own coordinates 32 + .. as c1).
-  __device__ __forceinline__ void hpass_split(int l, double (&h0)[RR], double (&h1)[RB + 4],
-                                              double a0, double b0, double a1, double b1,
-                                              double (&wa)[4], double (&wb)[4]) const {
-    const double aB = shfl(a1, l & 15), bB = shfl(b1, l & 15);
-    const double aC = shfl(a1, 16 + (l >> 4)), bC = shfl(b1, 16 + (l >> 4));
-    const double* G = rowv;
-    const double* DX = rowv + LD;
-    const double* U = rowv + 2 * LD;
-    const int rB0 = 26 * (l >> 4), rC0 = l & 15;
-    const double* GB = G + rB0;
-    const double* XB = DX + rB0;
-    const double* UB = U + rB0;
-    double wbb[4] = {0.0, 0.0, 0.0, 0.0}, wc[2] = {0.0, 0.0};
-#pragma unroll
-    for (int i = 0; i < RR; i += 2) {  // A register rows (broadcast row values)
-      const double2 g2 = *reinterpret_cast<const double2*>(G + i);
-      const double2 x2 = *reinterpret_cast<const double2*>(DX + i);
-      const double2 u2 = *reinterpret_cast<const double2*>(U + i);
-      h0[i] = fma(x2.x, a0, fma(u2.x, b0, h0[i]));
-      h0[i + 1] = fma(x2.y, a0, fma(u2.y, b0, h0[i + 1]));
-      wa[i & 3] = fma(h0[i], g2.x, wa[i & 3]);
-      wa[(i + 1) & 3] = fma(h0[i + 1], g2.y, wa[(i + 1) & 3]);
-    }
-#pragma unroll
-    for (int t = 0; t < RB; t += 2) {  // B register rows (two rows per half-warp)
-      const double2 g2 = *reinterpret_cast<const double2*>(GB + t);
-      const double2 x2 = *reinterpret_cast<const double2*>(XB + t);
-      const double2 u2 = *reinterpret_cast<const double2*>(UB + t);
-      h1[t] = fma(x2.x, aB, fma(u2.x, bB, h1[t]));
-      h1[t + 1] = fma(x2.y, aB, fma(u2.y, bB, h1[t + 1]));
-      wbb[t & 3] = fma(h1[t], g2.x, wbb[t & 3]);
-      wbb[(t + 1) & 3] = fma(h1[t + 1], g2.y, wbb[(t + 1) & 3]);
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {  // the C rows: 16 consecutive rows per load (one wavefront)
-      const int r = rC0 + 16 * t;
-      h1[RB + t] = fma(DX[r], aC, fma(U[r], bC, h1[RB + t]));
-      wc[t & 1] = fma(h1[RB + t], G[r], wc[t & 1]);
-    }
-    // Tensor Memory rows in groups of 4 (A rows RR.., then B rows RB..): the
-    // next group's loads are issued while this one is updated and stored
-    tmem::wait_st();
-#pragma unroll
-    for (int gi = 0; gi < (NTA + NTB) / 4; ++gi) {
-      const bool isA = gi < NTA / 4;
-      const int r0 = isA ? RR + 4 * gi : RB + 4 * (gi - NTA / 4);  // row (A) / step (B)
-      const double* Gp = isA ? G + r0 : GB + r0;
-      const double* Xp = isA ? DX + r0 : XB + r0;
-      const double* Up = isA ? U + r0 : UB + r0;
-      const double ca = isA ? a0 : aB, cb = isA ? b0 : bB;
-      double gr[4], xr[4], ur[4];
-#pragma unroll
-      for (int r = 0; r < 4; r += 2) {
-        const double2 g2 = *reinterpret_cast<const double2*>(Gp + r);
-        const double2 x2 = *reinterpret_cast<const double2*>(Xp + r);
-        const double2 u2 = *reinterpret_cast<const double2*>(Up + r);
-        gr[r] = g2.x, gr[r + 1] = g2.y;
-        xr[r] = x2.x, xr[r + 1] = x2.y;
-        ur[r] = u2.x, ur[r + 1] = u2.y;
-      }
-      const uint32_t ta = tm + 8 * gi;
-      tmem::D2 e[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) tmem::ld2(ta + 2 * r, e[r]);
-      tmem::wait_ld_n(e);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const double v = fma(xr[r], ca, fma(ur[r], cb, e[r].v()));
-        tmem::st2(ta + 2 * r, v);
-        if (isA) {
-          wa[(r0 + r - RR) & 3] = fma(v, gr[r], wa[(r0 + r - RR) & 3]);
-        } else {
-          wbb[(r0 + r) & 3] = fma(v, gr[r], wbb[(r0 + r) & 3]);
-        }
-      }
-    }
-    wb[0] = (wbb[0] + wbb[1]) + (wbb[2] + wbb[3]);
-    wb[1] = wc[0] + wc[1];
-  }
-  // w for this lane's coordinate c1 (lanes 0..17) from the split partials:
-  // column 32 + l is the sum of the two half-warp partials of lanes l, l ^ 16;
-  // columns 48 / 49 sum over the 16 lanes of the lower / upper half and go
-  // to their owners, lanes 16 / 17
-  __device__ __forceinline__ double split_w1(int l, const double (&wb)[4]) const {
-    const double wB = wb[0] + shfl_xor(wb[0], 16);
-    double wC = wb[1];
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) wC += shfl_xor(wC, o);
-    const double wCo = shfl(wC, (l & 1) << 4);
-    return l < 16 ? wB : (l < 18 ? wCo : 0.0);
-  }
-
   __device__ void run(const BfgsArgs& A, long long s, int l) {
     const int d = D > 0 ? D : A.d;
     const int nt = Obj::nterms(d);
     const int c0 = 64 * wi + l, c1 = c0 + 32;
     const bool own0 = W == 1 || c0 < d, own1 = c1 < d;
-    // SPLIT: h0 = A rows, h1 = B rows 0..RB-1 then the C rows; BLK3: h1 = the
-    // block's register rows [RR][3] then the C rows
+    // h0 / h1: rows 0..RR-1 of the columns c0 / c1; TM: h1 = the block's
+    // register rows [RR][3] then the 4 C rows
     double h0[H0N], h1[H1N];
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;  // pending rank-2 coefficients
     double x0 = 0.0, x1 = 0.0, p0 = 0.0, p1 = 0.0, g0 = 0.0, g1 = 0.0;
@@ -634,24 +523,6 @@ struct WideStart {
       rowv[4 * LD + 2 * c0 + 1] = 0.0;
       rowv[4 * LD + 2 * c1] = 0.0;
       rowv[4 * LD + 2 * c1 + 1] = 0.0;
-    } else if constexpr (SPLIT) {
-      const int cB = 32 + (l & 15), rB0 = 26 * (l >> 4), cC = 48 + (l >> 4), rC0 = l & 15;
-#pragma unroll
-      for (int i = 0; i < RR; ++i) h0[i] = i == c0 ? 1.0 : 0.0;
-#pragma unroll
-      for (int t = 0; t < RB; ++t) h1[t] = rB0 + t == cB ? 1.0 : 0.0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) h1[RB + t] = rC0 + 16 * t == cC ? 1.0 : 0.0;
-      // TMEM: A rows RR.. at columns [0, 2 NTA), B rows RB.. after them
-#pragma unroll
-      for (int i = RR; i < D; i += 4)
-        tmem::st4d(tm + 2 * (i - RR), i == c0 ? 1.0 : 0.0, i + 1 == c0 ? 1.0 : 0.0,
-                   i + 2 == c0 ? 1.0 : 0.0, i + 3 == c0 ? 1.0 : 0.0);
-#pragma unroll
-      for (int t = RB; t < 26; t += 4)
-        tmem::st4d(tm + 2 * NTA + 2 * (t - RB), rB0 + t == cB ? 1.0 : 0.0,
-                   rB0 + t + 1 == cB ? 1.0 : 0.0, rB0 + t + 2 == cB ? 1.0 : 0.0,
-                   rB0 + t + 3 == cB ? 1.0 : 0.0);
     } else {
 #pragma unroll
       for (int i = 0; i < RR; ++i) {
@@ -839,10 +710,6 @@ struct WideStart {
         static_assert(BLK3 || RR % 2 == 0, "register rows in pairs");
         if constexpr (BLK3) {
           hpass_blk3(l, h1, a1, b1, w0, w1);
-        } else if constexpr (SPLIT) {
-          hpass_split(l, h0, h1, a0, b0, a1, b1, wa, wb);
-          w0 = (wa[0] + wa[1]) + (wa[2] + wa[3]);
-          w1 = split_w1(l, wb);
         } else {
 #pragma unroll
         for (int i = 0; i < RR; i += 2) {
@@ -1067,7 +934,7 @@ int launch_wide(BfgsArgs A, cudaStream_t s) {
   A.nalpha = kAlphaTable;
   const int threads = TM ? 32 * kTmWarps : kWideThreads;
   // per start: rowv only (TM: the H rows are in Tensor Memory), else the full slice
-  A.warp_doubles = TM ? (ZEUS_WIDE_LAYOUT == 1 ? 6 : 4) * 64 : wide_slot_doubles(A.d, RR, W);
+  A.warp_doubles = TM ? 6 * 64 : wide_slot_doubles(A.d, RR, W);
   const int starts_per_block = threads / 32 / W;
   const size_t smem =
       sizeof(double) * ((size_t)A.nalpha + (size_t)starts_per_block * A.warp_doubles);

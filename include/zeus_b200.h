@@ -109,7 +109,10 @@ int zeus_pso_init(int obj, int d, int64_t n, int64_t i0, uint64_t seed, double l
                   double upper, double *x, double *v, double *pbest, double *pval,
                   int64_t ld, double *cand, void *workspace, void *stream);
 /* update_swarm (pso.py:123-164) for 0-based sweep `sweep`, reading the
- * previous barrier's global best gX[d] (pso.py:143). */
+ * previous barrier's global best gX[d] (pso.py:143).  Sweep s draws r1, r2
+ * from the particle streams' positions 2d(s+1) .. 2d(s+2)-1 (after init's 2d
+ * draws); sweep = -1 draws from the streams' start (a swarm that was not made
+ * by init_swarm, fresh streams). */
 int zeus_pso_sweep(int obj, int d, int64_t n, int64_t i0, uint64_t seed, int sweep,
                    double w, double c1, double c2, double *x, double *v, double *pbest,
                    double *pval, int64_t ld, const double *gX, double *cand,

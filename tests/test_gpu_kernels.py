@@ -153,3 +153,26 @@ def test_hessian_update_guards(z):
     assert np.allclose(upd, np.diag([0.5, 1.0]), atol=1e-15)
     assert np.array_equal(z.hessian_update(np.eye(2), np.array([1.0, 0.0]),
                                            np.array([1.0, 0.0])), np.eye(2))
+
+
+def test_registered_objectives_on_dual_numbers(z, oracle):
+    """The registered functions are generic over float / Dual like the
+    reference's (objectives.py:33-113): the real part of a Dual evaluation is
+    the float evaluation bit for bit; the dual part is grad f . t; Ackley's
+    sqrt'(0) raises DomainError whatever the tangents (autodiff.py:207-213)."""
+    rng = np.random.default_rng(11)
+    for fn, dim, (lo, hi) in [(z.rosenbrock, 4, (-5.0, 5.0)), (z.rastrigin, 4, (-5.12, 5.12)),
+                              (z.ackley, 4, (-5.0, 5.0)), (z.goldstein_price, 2, (-2.0, 2.0))]:
+        for _ in range(5):
+            x = rng.uniform(lo, hi, dim).tolist()
+            t = rng.uniform(-1.0, 1.0, dim).tolist()
+            plain = fn(x)
+            dual = fn([z.Dual(v, w) for v, w in zip(x, t)])
+            assert dual.real == plain, fn.__name__
+            g = z.forward_gradient(fn, x)
+            assert dual.dual == pytest.approx(float(np.dot(g, t)), rel=1e-12, abs=1e-12)
+    assert z.ackley([0.0, 0.0]) == pytest.approx(0.0, abs=1e-12)
+    with pytest.raises(z.DomainError):
+        z.ackley([z.Dual(0.0, 1.0), z.Dual(0.0, 0.0)])
+    with pytest.raises(z.DomainError):
+        z.ackley([z.Dual(0.0, 0.0), z.Dual(0.0, 0.0)])

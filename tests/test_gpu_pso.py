@@ -212,3 +212,29 @@ def test_peer_exchange_matches_single_swarm(name, d, n, world, sweeps):
             for t in ("x", "v", "p"):
                 assert torch.equal(getattr(s, t)[:, :b - a], getattr(one, t)[:, a:b]), t
             assert torch.equal(s.pval[:b - a], one.pval[a:b])
+
+
+def test_update_swarm_from_fresh_streams(z):
+    """update_swarm on a swarm not made by init_swarm (fresh streams, offset
+    0): r1, r2 are the streams' first 2d draws, as in the reference
+    (pso.py:143-163, streams.py:40-54) -- checked against a host restatement
+    from ParticleStreams.generator(i)."""
+    x = np.array([[1.0, -2.0], [0.5, 3.0], [-4.0, 0.25]])
+    v = np.array([[0.4, -0.6], [0.1, 0.2], [-0.3, 0.05]])
+    fx = [z.rastrigin(r.tolist()) for r in x]
+    gi = int(np.argmin(fx))
+    state = z.SwarmState(positions=x.copy(), velocities=v.copy(), personal_best_pos=x.copy(),
+                         personal_best_val=np.array(fx), global_best_pos=x[gi].copy(),
+                         global_best_val=fx[gi])
+    params = z.PsoParams(w=0.5, c1_pso=1.2, c2_pso=1.5)
+    streams = z.make_start_streams(3, 3, 2)
+    z.update_swarm(state, z.rastrigin, params, streams)
+    ref = z.make_start_streams(3, 3, 2)
+    for i in range(3):
+        r = ref.generator(i).uniform(0.0, 1.0, 4)
+        r1, r2 = r[:2], r[2:]
+        vn = (0.5 * v[i] + (1.2 * r1) * (x[i] - x[i])) + (1.5 * r2) * (x[gi] - x[i])
+        assert np.array_equal(state.velocities[i], vn), i
+        assert np.array_equal(state.positions[i], x[i] + vn), i
+    # x = p = g: both attraction terms vanish (the reference's own check)
+    assert np.allclose(state.velocities[gi], 0.5 * v[gi], atol=1e-15)

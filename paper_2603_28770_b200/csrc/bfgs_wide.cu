@@ -971,16 +971,14 @@ struct WideLaunch {
     if constexpr (Obj::kId == ZEUS_OBJ_GOLDSTEIN_PRICE) {
       return set_error(ZEUS_ERR_UNSUPPORTED, "wide: goldstein_price is 2-D");
     } else {
-      // the BASELINE dimensions get kernels compiled for them (T50: d = 50;
-      // config 4: d = 100); any other 32 < d <= 128 runs the generic build
-      // d = 50: Rosenbrock / Rastrigin keep the H rows beyond the register
-      // rows in Tensor Memory (SM-cycles per start-iteration, TMEM / shared
-      // memory: Rosenbrock 556 / 628, Rastrigin 1,226 / 1,251); Ackley's
-      // two-accumulator line search needs the registers the TMEM access
-      // pattern takes (1,452 / 1,342), so it keeps the shared-memory rows
+      // the BASELINE dimensions get kernels compiled for them (T50 and
+      // config 3: d = 50; config 4: d = 100); any other 32 < d <= 128 runs
+      // the generic build.  d = 50: the block layout with the H elements
+      // beyond the register rows in Tensor Memory (SM-cycles per
+      // start-iteration, TMEM block layout / shared-memory rows: Rosenbrock
+      // 448 / 628, Rastrigin 1,062 / 1,251, Ackley 1,120 / 1,341)
 #ifndef ZEUS_WIDE_NO_TMEM
-      if constexpr (Obj::kId != ZEUS_OBJ_ACKLEY)
-        if (A.d == 50) return launch_wide<Obj, WideShape<Obj, 1>::RR_TM, 1, 50, true>(A, s);
+      if (A.d == 50) return launch_wide<Obj, WideShape<Obj, 1>::RR_TM, 1, 50, true>(A, s);
 #endif
       if (A.d == 50) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 50>(A, s);
       if (A.d <= 64) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 0>(A, s);

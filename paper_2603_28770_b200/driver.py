@@ -243,6 +243,13 @@ def _broadcast_best(per_run, bidx: int, owner: int, d: int, group, dev) -> BfgsO
                        status=STATUSES[int(r[d + 3])])
 
 
+def _stop_wave(cfg: ZeusConfig, required_c: int) -> int:
+    """First launch size of the parallel early-stop mode: the reference's
+    pool has `workers` runs in flight at a time (driver.py:184-201), and at
+    least required_c starts must run to reach the target."""
+    return max(int(required_c), int(cfg.workers), 1)
+
+
 def _gather_mode(gather) -> str:
     if gather is True or gather == "all":
         return "all"
@@ -329,7 +336,8 @@ def _zeus_run_devices(obj, cfg: ZeusConfig, devs, starts, within, t0) -> ZeusRes
             if n > 0:
                 x0 = c["x0"]
                 engine.run_bfgs(obj, x0.contiguous() if x0.stride(0) != x0.shape[1] else x0,
-                                params, out, dev, required_c=required_c, stop=stop)
+                                params, out, dev, required_c=required_c, stop=stop,
+                                wave=_stop_wave(cfg, required_c) if stop is not None else 0)
             c["ev"][2].record(c["stream"])
             best = torch.empty(2, dtype=torch.float64, device=dev)
             tallies = torch.zeros(4, dtype=torch.int64, device=dev)
@@ -547,7 +555,8 @@ def zeus_run(f: Callable[[Sequence], object], cfg: ZeusConfig, *, device=None,
         stop = (blk.counter, blk.flag)
     if n > 0:
         engine.run_bfgs(obj, x0.contiguous() if x0.stride(0) != x0.shape[1] else x0, params,
-                        out, dev, required_c=required_c, stop=stop)
+                        out, dev, required_c=required_c, stop=stop,
+                        wave=_stop_wave(cfg, required_c) if stop is not None else 0)
 
     ev_bfgs.record(stream)
     # ---- reduction (driver.py:250-251) on device

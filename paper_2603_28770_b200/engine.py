@@ -64,12 +64,15 @@ class BfgsBuffers:
             grad_evals=torch.empty(max(n, 1), dtype=torch.int32, device=device),
         )
 
-    def c_struct(self, n: int) -> _capi.BfgsOut:
+    def c_struct(self, n: int, lo: int = 0) -> _capi.BfgsOut:
+        """The C view of starts [lo, lo + n) (same row stride)."""
         return _capi.BfgsOut(
-            x_final=self.x_final.data_ptr(), ld_out=self.x_final.shape[1],
-            f_final=self.f_final.data_ptr(), grad_norm=self.grad_norm.data_ptr(),
-            iterations=self.iterations.data_ptr(), status=self.status.data_ptr(),
-            ls_trials=self.ls_trials.data_ptr(), grad_evals=self.grad_evals.data_ptr())
+            x_final=self.x_final.data_ptr() + 8 * lo, ld_out=self.x_final.shape[1],
+            f_final=self.f_final.data_ptr() + 8 * lo,
+            grad_norm=self.grad_norm.data_ptr() + 8 * lo,
+            iterations=self.iterations.data_ptr() + 4 * lo, status=self.status.data_ptr() + lo,
+            ls_trials=self.ls_trials.data_ptr() + 4 * lo,
+            grad_evals=self.grad_evals.data_ptr() + 4 * lo)
 
 
 def bfgs_params(theta: float, iter_bfgs: int, ls) -> _capi.BfgsParams:
@@ -80,13 +83,38 @@ def bfgs_params(theta: float, iter_bfgs: int, ls) -> _capi.BfgsParams:
 
 def run_bfgs(obj: int, x0: torch.Tensor, params: _capi.BfgsParams, out: BfgsBuffers,
              device, required_c: int = 0, stop=None,
-             ws: Optional[torch.Tensor] = None) -> None:
+             ws: Optional[torch.Tensor] = None, wave: int = 0) -> None:
     """Multistart BFGS over the SoA starts ``x0`` [d][n] (bfgs.py:80-156).
     ``stop`` = (counter, flag) as tensors or raw device addresses (the
-    cross-process StopBlock)."""
+    cross-process StopBlock).
+
+    ``wave`` > 0 (parallel early stop, driver.py:153-202): the starts run in
+    consecutive launches of wave, 2 wave, 4 wave, ... starts, like the
+    reference's pool that starts a run only when a worker frees up: once the
+    stop flag is set, the starts of later launches end at their first probe
+    -- status stopped, iterations 0, grad_norm inf, f_final = f(x0), the
+    reference's never-started outcome -- instead of all N running at once."""
     d, n = x0.shape
     if n == 0:
         return
+    if stop is not None and 0 < wave < n:
+        if ws is None:
+            ws = _device.workspace(_capi.lib().zeus_bfgs_workspace_bytes(d, n)
+                                   if isinstance(obj, int) else
+                                   _capi.lib().zeus_user_bfgs_workspace_bytes(), device)
+        lo, size = 0, wave
+        while lo < n:
+            m = min(size, n - lo)
+            _run_bfgs_slice(obj, x0, params, out, device, required_c, stop, ws, lo, m)
+            lo += m
+            size *= 2
+        return
+    _run_bfgs_slice(obj, x0, params, out, device, required_c, stop, ws, 0, n)
+
+
+def _run_bfgs_slice(obj, x0, params, out, device, required_c, stop, ws, lo, n):
+    d = x0.shape[0]
+    xs = x0.narrow(1, lo, n)
     L = _capi.lib()
     counter = flag = None
     if stop is not None:
@@ -96,15 +124,15 @@ def run_bfgs(obj: int, x0: torch.Tensor, params: _capi.BfgsParams, out: BfgsBuff
             ws = _device.workspace(L.zeus_user_bfgs_workspace_bytes(), device)
         sp = _device.stream_ptr(device)
         obj.bind(sp)
-        _capi.check(L.zeus_user_bfgs(obj.handle, n, x0.data_ptr(), x0.stride(0), params,
-                                     int(required_c), counter, flag, out.c_struct(n),
+        _capi.check(L.zeus_user_bfgs(obj.handle, n, xs.data_ptr(), xs.stride(0), params,
+                                     int(required_c), counter, flag, out.c_struct(n, lo),
                                      ws.data_ptr(), sp), "bfgs (user objective)")
         LAUNCHES[0] += 1
         return
     if ws is None:
         ws = _device.workspace(L.zeus_bfgs_workspace_bytes(d, n), device)
-    _capi.check(L.zeus_bfgs(obj, d, n, x0.data_ptr(), x0.stride(0), params, int(required_c),
-                            counter, flag, out.c_struct(n), ws.data_ptr(),
+    _capi.check(L.zeus_bfgs(obj, d, n, xs.data_ptr(), xs.stride(0), params, int(required_c),
+                            counter, flag, out.c_struct(n, lo), ws.data_ptr(),
                             _device.stream_ptr(device)), "bfgs")
     # small d: thread-per-start tier, warp-per-start tier for starts still
     # running at k1t, CTA-team tier for those still running at k1 (bfgs.cu)

@@ -106,6 +106,24 @@ def test_device_early_stop_every_kernel(z, name, d, n):
     assert np.all(np.isinf(gn[(st == 2) & (k == 0)]))
 
 
+def test_device_early_stop_skips_most_work(z):
+    """The reference's pool starts a run only when a worker frees up, so with
+    required_c = 1 almost every start is skipped (test_driver.py:185-192);
+    the launches of doubling size reproduce that: starts of launches after
+    the flag end at their first probe (iterations 0, |g| = inf, f = f(x0))."""
+    cfg = z.ZeusConfig(N=400, dim=2, range=(-4.0, 4.0), iter_pso=0, iter_bfgs=200,
+                       required_c=1, seed=3, workers=2)
+    res = z.zeus_run(z.rastrigin, cfg)
+    st, k = res.per_run.status_codes, res.per_run.iterations
+    stopped = st == 2
+    assert stopped.sum() > 300
+    assert k[stopped].sum() <= stopped.sum() + 2 * 200
+    never = stopped & (k == 0)
+    assert np.all(np.isinf(res.per_run.grad_norm[never]))
+    f0 = [z.rastrigin(x.tolist()) for x in res.per_run.x_final[never][:5]]
+    assert np.array_equal(res.per_run.f_final[never][:5], f0)
+
+
 def test_deterministic_mode_disables_early_stop(z):
     cfg = z.ZeusConfig(N=20, dim=2, range=(-5.12, 5.12), iter_pso=1, iter_bfgs=200,
                        required_c=1, seed=4, workers=2, deterministic=True)

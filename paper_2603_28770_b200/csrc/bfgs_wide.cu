@@ -123,6 +123,21 @@ struct WideShape {
 #else
   static constexpr int RR_TM = kRosen ? 7 : 5;
 #endif
+  // d = 20 (config 5, sequential folds): trials per chunk and resident
+  // 2-warp blocks per SM, measured (SM-cycles per start-iteration, CH / MINB):
+  // Rastrigin 960 (2 / 6), 878 (3 / 6), 909 (4 / 6), 1,026 (4 / 8);
+  // Rosenbrock 314 (2 / 6), 295 (2 / 8), 322 (3 / 6); the warp kernel
+  // (bfgs_warp.cuh) it replaces: 1,348 / 512
+#ifdef ZEUS_WIDE_SEQ_CH
+  static constexpr int SEQ_CH = ZEUS_WIDE_SEQ_CH;
+#else
+  static constexpr int SEQ_CH = kRosen ? 2 : 3;
+#endif
+#ifdef ZEUS_WIDE_SEQ_MINB
+  static constexpr int SEQ_MINB = ZEUS_WIDE_SEQ_MINB;
+#else
+  static constexpr int SEQ_MINB = kRosen ? 8 : 6;
+#endif
 #ifdef ZEUS_WIDE_SMEM_STEP
   static constexpr int SR = ZEUS_WIDE_SMEM_STEP;
 #else
@@ -157,11 +172,21 @@ struct WideStart {
   // owners through the spare rowv row.  RR block rows in registers, the
   // other NT3 in Tensor Memory.
   static constexpr bool BLK3 = TM;
+  // SEQ (one warp, d <= 32: config 5's d = 20): objective values are folded in
+  // the reference's sequential order (a Python left fold, objectives.py:
+  // 40-85) instead of a tree, so f at identical x is the reference's f bit
+  // for bit (Rosenbrock) and Armijo decisions at the noise floor |g| ~ theta
+  // follow the reference's; the terms go through the spare rowv row and lane
+  // q folds value q.
+  static constexpr bool SEQ = W == 1 && D > 0 && D <= 32;
+  // SEQ: trials per chunk -- the CH folds run in parallel lanes, so a wider
+  // chunk means fewer sequential fold rounds per iteration (WideShape)
+  static constexpr int kSeqCH = NA == 1 ? WideShape<Obj, 1>::SEQ_CH : 1;
   static_assert(!TM || (W == 1 && D == 50), "TMEM kernel: the d = 50 block layout");
   static constexpr int NT3 = BLK3 ? 25 - RR : 0;  // block rows in TMEM
   static_assert(!BLK3 || (NT3 % 2 == 0 && 6 * NT3 <= kTmAlloc), "block layout");
   static constexpr int H0N = BLK3 ? 1 : RR;  // register arrays of the pass
-  static constexpr int H1N = BLK3 ? 3 * RR + 4 : RR;
+  static constexpr int H1N = BLK3 ? 3 * RR + 4 : SEQ ? 1 : RR;  // SEQ: no column c1
   uint32_t tm = 0;     // TM: this thread's TMEM column base (lane = its thread)
   double* Hs;          // [d - RR][LD] rows RR.. of every column of the start
   double* rowv;        // [4][64 W]: g' | dx_prev | u_prev | w (TM); TM: + [64][2] (a, b)
@@ -205,6 +230,37 @@ struct WideStart {
       }
     }
   }
+  // SEQ: values v[0 .. nv) (nv <= 4: rows 3..4 of the slot hold 4 x 32 terms), each
+  // lane's term of value q, folded as init[q] + t_0 + t_1 + ... + t_{nt-1}
+  // (left to right), identical in every lane
+  __device__ __forceinline__ void seq_fold(double v[8], const double init[8], int nv, int l,
+                                           int nt) const {
+    double* T = rowv + 3 * LD;
+    __syncwarp();  // the previous fold's readers are done
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < nv && l < nt) T[q * 32 + l] = v[q];
+    __syncwarp();
+    double sacc = 0.0;
+    if (l < nv) {
+      double t[D > 0 ? D : 1];
+#pragma unroll
+      for (int j = 0; j < (D > 0 ? D : 1); ++j) t[j] = j < nt ? T[l * 32 + j] : 0.0;
+      sacc = init[0];
+#pragma unroll
+      for (int q = 1; q < 4; ++q)
+        if (l == q) sacc = init[q];
+#pragma unroll
+      for (int j = 0; j < (D > 0 ? D : 1); ++j) {
+        if (j >= nt) break;
+        sacc = sacc + t[j];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < nv) v[q] = shfl(sacc, q);
+  }
+
   // v[0..3] summed over the team (one transpose-reduce: 10 shuffles)
   __device__ __forceinline__ void team_sum4(double v[8], int l) {
     warp_sum4(v);
@@ -365,7 +421,7 @@ struct WideStart {
       }
     }
     g0 = 0.0;
-    if (W == 1 || c0 < d) g0 = Obj::grad_from_tan(LT{c0, tA[0], tA[1], prevA}, c0, d, acc, err);
+    if ((W == 1 && D > 32) || c0 < d) g0 = Obj::grad_from_tan(LT{c0, tA[0], tA[1], prevA}, c0, d, acc, err);
     g1 = 0.0;
     if (c1 < d) g1 = Obj::grad_from_tan(LT{c1, tB[0], tB[1], prevB}, c1, d, acc, err);
   }
@@ -483,7 +539,7 @@ struct WideStart {
     const int d = D > 0 ? D : A.d;
     const int nt = Obj::nterms(d);
     const int c0 = 64 * wi + l, c1 = c0 + 32;
-    const bool own0 = W == 1 || c0 < d, own1 = c1 < d;
+    const bool own0 = (W == 1 && D > 32) || c0 < d, own1 = c1 < d;
     // h0 / h1: rows 0..RR-1 of the columns c0 / c1; TM: h1 = the block's
     // register rows [RR][3] then the 4 C rows
     double h0[H0N], h1[H1N];
@@ -527,7 +583,7 @@ struct WideStart {
 #pragma unroll
       for (int i = 0; i < RR; ++i) {
         h0[i] = i == c0 ? 1.0 : 0.0;
-        h1[i] = i == c1 ? 1.0 : 0.0;
+        if constexpr (!SEQ) h1[i] = i == c1 ? 1.0 : 0.0;
       }
       for (int i = RR; i < d; ++i) {
         Hs[(i - RR) * LD + c0] = i == c0 ? 1.0 : 0.0;
@@ -553,7 +609,20 @@ struct WideStart {
       lane_tan<FastMath>(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB, oor);
       if (team_any(oor)) lane_tan_precise(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB);
 #pragma unroll
-      for (int a = 0; a < NA; ++a) acc[a] = Obj::init(a, d) + team_sum(sv[a], l);
+      if constexpr (SEQ) {
+        double v[8], in[8];
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+          v[a] = sv[a];
+          in[a] = Obj::init(a, d);
+        }
+        seq_fold(v, in, NA, l, nt);
+#pragma unroll
+        for (int a = 0; a < NA; ++a) acc[a] = v[a];
+      } else {
+#pragma unroll
+        for (int a = 0; a < NA; ++a) acc[a] = Obj::init(a, d) + team_sum(sv[a], l);
+      }
       bool ferr = false;
       f0 = Obj::finish(acc, d, ferr);
       if (A.stop_flag && team_any(*(volatile int*)A.stop_flag != 0)) {
@@ -592,7 +661,7 @@ struct WideStart {
 #ifdef ZEUS_WIDE_CH  // (variant builds; kept only where a slot for g.p remains)
         constexpr int CH = ZEUS_WIDE_CH * NA < 8 ? ZEUS_WIDE_CH : WideShape<Obj, W>::CH;
 #else
-        constexpr int CH = WideShape<Obj, W>::CH;
+        constexpr int CH = SEQ ? kSeqCH : WideShape<Obj, W>::CH;
 #endif
         static_assert(CH * NA <= 8, "one reduction per chunk");
         for (int t0 = 0;; t0 += CH) {
@@ -617,7 +686,14 @@ struct WideStart {
 #pragma unroll
           for (int q = 0; q < 8; ++q) v[q] = q < CH * NA ? sc[q % CH][q / CH] : 0.0;
           static_assert(CH * NA < 8, "a slot for g.p");
-          if (t0 == 0) {  // g.p rides with the first chunk (slot CH * NA)
+          if constexpr (SEQ) {
+            static_assert(!SEQ || CH * NA <= 4, "four fold rows");
+            if (t0 == 0) ddir = warp_sum(pd_part);  // (a tree, like OpenBLAS's ddot)
+            double in[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) in[q] = Obj::init(q / CH, d);
+            seq_fold(v, in, CH * NA, l, nt);
+          } else if (t0 == 0) {  // g.p rides with the first chunk (slot CH * NA)
             v[CH * NA] = pd_part;
             if constexpr (CH * NA + 1 <= 4) {
               team_sum4(v, l);
@@ -638,7 +714,7 @@ struct WideStart {
           for (int c = 0; c < CH; ++c) {
             double ab[NA];
 #pragma unroll
-            for (int a = 0; a < NA; ++a) ab[a] = Obj::init(a, d) + v[a * CH + c];
+            for (int a = 0; a < NA; ++a) ab[a] = SEQ ? v[a * CH + c] : Obj::init(a, d) + v[a * CH + c];
             const bool valid = t0 + c <= A.iter_ls;
             bool ferr = false;
             if constexpr (NA > 1) {  // Ackley: exp / sqrt only for trials that exist
@@ -659,7 +735,8 @@ struct WideStart {
                 f_new = fb[c];
                 alpha = al[c];
 #pragma unroll
-                for (int a = 0; a < NA; ++a) acc_new[a] = Obj::init(a, d) + v[a * CH + c];
+                for (int a = 0; a < NA; ++a)
+                  acc_new[a] = SEQ ? v[a * CH + c] : Obj::init(a, d) + v[a * CH + c];
               }
             }
             t_acc = t0 + src;
@@ -717,13 +794,15 @@ struct WideStart {
           const double2 x2 = *reinterpret_cast<const double2*>(DX + i);
           const double2 u2 = *reinterpret_cast<const double2*>(U + i);
           h0[i] = fma(x2.x, a0, fma(u2.x, b0, h0[i]));
-          h1[i] = fma(x2.x, a1, fma(u2.x, b1, h1[i]));
           h0[i + 1] = fma(x2.y, a0, fma(u2.y, b0, h0[i + 1]));
-          h1[i + 1] = fma(x2.y, a1, fma(u2.y, b1, h1[i + 1]));
           wa[i & 3] = fma(h0[i], g2.x, wa[i & 3]);
-          wb[i & 3] = fma(h1[i], g2.x, wb[i & 3]);
           wa[(i + 1) & 3] = fma(h0[i + 1], g2.y, wa[(i + 1) & 3]);
-          wb[(i + 1) & 3] = fma(h1[i + 1], g2.y, wb[(i + 1) & 3]);
+          if constexpr (!SEQ) {  // (SEQ: d <= 32, no second column)
+            h1[i] = fma(x2.x, a1, fma(u2.x, b1, h1[i]));
+            h1[i + 1] = fma(x2.y, a1, fma(u2.y, b1, h1[i + 1]));
+            wb[i & 3] = fma(h1[i], g2.x, wb[i & 3]);
+            wb[(i + 1) & 3] = fma(h1[i + 1], g2.y, wb[(i + 1) & 3]);
+          }
         }
         {
           // rows RR.. from shared memory, SR per step with every load issued
@@ -874,7 +953,9 @@ struct WideStart {
 
 template <class Obj, int RR, int W, int D, bool TM>
 __global__ void __launch_bounds__(TM ? 32 * kTmWarps : kWideThreads,
-                                  TM ? WideShape<Obj, 1>::TM_CTAS : WideShape<Obj, W>::MINB)
+                                  TM ? WideShape<Obj, 1>::TM_CTAS
+                                     : (W == 1 && D > 0 && D <= 32) ? WideShape<Obj, 1>::SEQ_MINB
+                                                                    : WideShape<Obj, W>::MINB)
     bfgs_wide_kernel(BfgsArgs A) {
   extern __shared__ double sm[];
   const int l = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -934,7 +1015,8 @@ int launch_wide(BfgsArgs A, cudaStream_t s) {
   A.nalpha = kAlphaTable;
   const int threads = TM ? 32 * kTmWarps : kWideThreads;
   // per start: rowv only (TM: the H rows are in Tensor Memory), else the full slice
-  A.warp_doubles = TM ? 6 * 64 : wide_slot_doubles(A.d, RR, W);
+  // (d <= 32: 64 more doubles, the SEQ folds' second scratch row)
+  A.warp_doubles = TM ? 6 * 64 : wide_slot_doubles(A.d, RR, W) + (A.d <= 32 ? 64 : 0);
   const int starts_per_block = threads / 32 / W;
   const size_t smem =
       sizeof(double) * ((size_t)A.nalpha + (size_t)starts_per_block * A.warp_doubles);
@@ -980,6 +1062,8 @@ struct WideLaunch {
 #ifndef ZEUS_WIDE_NO_TMEM
       if (A.d == 50) return launch_wide<Obj, WideShape<Obj, 1>::RR_TM, 1, 50, true>(A, s);
 #endif
+      if constexpr (Obj::kId != ZEUS_OBJ_ACKLEY)  // config 5 (Ackley: the warp kernel)
+        if (A.d == 20) return launch_wide<Obj, 20, 1, 20>(A, s);
       if (A.d == 50) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 50>(A, s);
       if (A.d <= 64) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 0>(A, s);
       if (A.d == 100) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2, 100>(A, s);
@@ -991,7 +1075,8 @@ struct WideLaunch {
 }  // namespace
 
 bool bfgs_wide_covers(int obj, int d) {
-  return obj != ZEUS_OBJ_GOLDSTEIN_PRICE && d > 32 && d <= 128;
+  return obj != ZEUS_OBJ_GOLDSTEIN_PRICE &&
+         ((d > 32 && d <= 128) || (d == 20 && obj != ZEUS_OBJ_ACKLEY));
 }
 
 int launch_bfgs_wide(int obj, BfgsArgs A, cudaStream_t s) {

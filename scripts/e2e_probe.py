@@ -16,3 +16,12 @@ for s in range(6):
     rows.append(((t1 - t0) * 1e3, r.device_time * 1e3, r.stats.pso_time * 1e3, r.stats.bfgs_time * 1e3, r.stats.reduce_time * 1e3))
 a = np.array(rows).mean(0)
 print("wall %.3f device %.3f (pso %.3f bfgs %.3f reduce %.3f) -> outside device window %.3f ms" % (a[0], a[1], a[2], a[3], a[4], a[0] - a[1]))
+if len(sys.argv) > 1 and sys.argv[1] == "profile":  # where the host time goes
+    import cProfile, pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    for s in range(4):
+        flush.fill_(1.0); torch.cuda.synchronize()
+        z.zeus_run(z.rastrigin, cfg(50 + s))
+    pr.disable()
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(25)

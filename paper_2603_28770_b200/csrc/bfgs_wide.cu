@@ -50,10 +50,10 @@ namespace zeus {
 namespace {
 
 constexpr int kWideThreads = 64;  // block: 2 warps = 2 starts (W = 1) or 1 start (W = 2)
-// TMEM kernel (d = 50): CTAs of 4 warps (one start each, warp w on TMEM lane
-// quarter w), each allocating 128 TMEM columns; WideShape::TM_CTAS per SM
+// TMEM kernels: CTAs of 4 warps (warp w on TMEM lane quarter w) -- four
+// starts of one warp (d = 50) or two starts of two warps (d = 100) --
+// WideShape::TM_CTAS per SM, the SM's 512 TMEM columns split between them
 constexpr int kTmWarps = 4;
-constexpr int kTmAlloc = 128;  // columns allocated per CTA = columns per warp
 
 // Term j's coordinate accessor: x(j) -> xj, x(j + 1) -> xj1 (Rosenbrock's
 // neighbour); objectives only ever ask for these two.
@@ -116,12 +116,13 @@ struct WideShape {
 #ifdef ZEUS_WIDE_TM_CTAS
   static constexpr int TM_CTAS = ZEUS_WIDE_TM_CTAS;
 #else
-  static constexpr int TM_CTAS = 4;
+  static constexpr int TM_CTAS = W > 1 ? 2 : 4;  // d = 100: 8 warps, 256 columns per CTA
 #endif
+  static constexpr int TM_COLS = 512 / TM_CTAS;  // TMEM columns per CTA (= per warp)
 #ifdef ZEUS_WIDE_RR_TM
   static constexpr int RR_TM = ZEUS_WIDE_RR_TM;
 #else
-  static constexpr int RR_TM = kRosen ? 7 : 5;
+  static constexpr int RR_TM = W > 1 ? 8 : (kRosen ? 7 : 5);
 #endif
   // d = 20 (config 5, sequential folds): trials per chunk and resident
   // 2-warp blocks per SM, measured (SM-cycles per start-iteration, CH / MINB):
@@ -182,11 +183,20 @@ struct WideStart {
   // SEQ: trials per chunk -- the CH folds run in parallel lanes, so a wider
   // chunk means fewer sequential fold rounds per iteration (WideShape)
   static constexpr int kSeqCH = NA == 1 ? WideShape<Obj, 1>::SEQ_CH : 1;
-  static_assert(!TM || (W == 1 && D == 50), "TMEM kernel: the d = 50 block layout");
-  static constexpr int NT3 = BLK3 ? 25 - RR : 0;  // block rows in TMEM
-  static_assert(!BLK3 || (NT3 % 2 == 0 && 6 * NT3 <= kTmAlloc), "block layout");
+  static_assert(!TM || (W == 1 && D == 50) || (W == 2 && D == 100),
+                "TMEM kernels: the block layout at d = 50 (one warp) / 100 (two warps)");
+  // d = 100 (W = 2): lane L = 32 w + l keeps rows 2 r + q (r = 0..49, q =
+  // bit 4 of l) of columns 3 p .. 3 p + 2, p = 16 w + (l & 15) (columns
+  // 0..95), plus rows (L & 15) + 16 t (t = 0..6) of column 96 + (L >> 4)
+  static constexpr int NRW = D / 2;              // block rows per lane
+  static constexpr int XT = (D + 15) / 16;       // rows per lane of the extra columns
+  static constexpr int NT3 = BLK3 ? NRW - RR : 0;  // block rows in TMEM
+  static constexpr int TMA = WideShape<Obj, W>::TM_COLS;
+  static_assert(!BLK3 || (NT3 % 2 == 0 && 6 * NT3 <= TMA), "block layout");
+  // several starts per CTA (d = 100): per-start named barriers
+  static constexpr bool MULTI = TM && W > 1;
   static constexpr int H0N = BLK3 ? 1 : RR;  // register arrays of the pass
-  static constexpr int H1N = BLK3 ? 3 * RR + 4 : SEQ ? 1 : RR;  // SEQ: no column c1
+  static constexpr int H1N = BLK3 ? 3 * RR + XT : SEQ ? 1 : RR;  // SEQ: no column c1
   uint32_t tm = 0;     // TM: this thread's TMEM column base (lane = its thread)
   double* Hs;          // [d - RR][LD] rows RR.. of every column of the start
   double* rowv;        // [4][64 W]: g' | dx_prev | u_prev | w (TM); TM: + [64][2] (a, b)
@@ -194,6 +204,7 @@ struct WideStart {
   const double* atab;  // block alpha table
   int wi = 0;          // warp index within the start (0 .. W-1)
   int slot = 0;        // reduction double-buffer
+  int bar_id = 0;      // MULTI: the start's named barrier (1 + its slot in the CTA)
 
   __device__ __forceinline__ double alpha_at(const BfgsArgs& A, int t) const {
     if (t < A.nalpha) return atab[t];
@@ -204,10 +215,29 @@ struct WideStart {
 
   // ---- team primitives (W == 1: the warp itself) -------------------------
   __device__ __forceinline__ void team_sync() const {
-    if constexpr (W > 1) __syncthreads(); else __syncwarp();
+    if constexpr (MULTI) {
+      asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "n"(32 * W) : "memory");
+    } else if constexpr (W > 1) {
+      __syncthreads();
+    } else {
+      __syncwarp();
+    }
   }
   __device__ __forceinline__ bool team_any(bool b) const {
-    if constexpr (W > 1) return __syncthreads_or(b); else return __any_sync(kFull, b);
+    if constexpr (MULTI) {
+      int r;
+      asm volatile(
+          "{\n .reg .pred p, q;\n setp.ne.s32 p, %1, 0;\n bar.red.or.pred q, %2, %3, p;\n"
+          " selp.s32 %0, 1, 0, q;\n}\n"
+          : "=r"(r)
+          : "r"((int)b), "r"(bar_id), "n"(32 * W)
+          : "memory");
+      return r != 0;
+    } else if constexpr (W > 1) {
+      return __syncthreads_or(b);
+    } else {
+      return __any_sync(kFull, b);
+    }
   }
   // 8 values summed over the team, identical in every lane of every warp
   // (warp transpose-reduce, then the W warp totals in warp order)
@@ -220,7 +250,7 @@ struct WideStart {
 #pragma unroll
         for (int q = 0; q < 8; ++q) r[wi * 8 + q] = v[q];
       }
-      __syncthreads();
+      team_sync();
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         double s = r[q];
@@ -271,7 +301,7 @@ struct WideStart {
 #pragma unroll
         for (int q = 0; q < 4; ++q) r[wi * 8 + q] = v[q];
       }
-      __syncthreads();
+      team_sync();
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         double s = r[q];
@@ -292,7 +322,7 @@ struct WideStart {
         r[wi * 8] = v[0];
         r[wi * 8 + 1] = v[1];
       }
-      __syncthreads();
+      team_sync();
       double s0 = r[0], s1 = r[1];
 #pragma unroll
       for (int w = 1; w < W; ++w) {
@@ -309,7 +339,7 @@ struct WideStart {
       double* r = xch + slot * 8 * W;
       slot ^= 1;
       if (l == 0) r[wi * 8] = v;
-      __syncthreads();
+      team_sync();
       double s = r[0];
 #pragma unroll
       for (int w = 1; w < W; ++w) s += r[w * 8];
@@ -416,7 +446,7 @@ struct WideStart {
       if constexpr (W > 1) {      // term 64w - 1: the previous warp's lane 31 c1 term
         double* tb = xch + 16 * W + 2 * W;
         if (l == 31) tb[wi] = tB[1];
-        __syncthreads();
+        team_sync();
         if (l == 0 && wi > 0) prevA = tb[wi - 1];
       }
     }
@@ -446,7 +476,7 @@ struct WideStart {
           xb[wi] = x0;
           pb[wi] = p0;
         }
-        __syncthreads();
+        team_sync();
         if (l == 31) {
           nx1 = wi + 1 < W ? xb[wi + 1] : 0.0;
           np1 = wi + 1 < W ? pb[wi + 1] : 0.0;
@@ -457,18 +487,20 @@ struct WideStart {
 
   // BLK3 pass: the lazy rank-2 update of the lane's 79 elements and their
   // matvec partials; returns w = H g' for the lane's coordinates c0, c1.
-  __device__ __forceinline__ void hpass_blk3(int l, double (&h1)[H1N], double a1, double b1,
-                                             double& w0, double& w1) const {
-    const int q = l >> 4, pq = l & 15, rC0 = l & 15;
-    const double* CF = rowv + 4 * LD + 6 * pq;  // (a, b) of columns 3 p + k
+  __device__ __forceinline__ void hpass_blk3(int l, double (&h1)[H1N], int c0, int c1,
+                                             bool own1, double& w0, double& w1) const {
+    const int L = 32 * wi + l;
+    const int q = (l >> 4) & 1, pq = 16 * wi + (l & 15), rC0 = L & 15, cX = 48 * W + (L >> 4);
+    const double* CF = rowv + 4 * LD;  // (a, b) by column
     double a[3], b[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const double2 ab = *reinterpret_cast<const double2*>(CF + 2 * k);
+      const double2 ab = *reinterpret_cast<const double2*>(CF + 2 * (3 * pq + k));
       a[k] = ab.x;
       b[k] = ab.y;
     }
-    const double aC = shfl(a1, 16 + (l >> 4)), bC = shfl(b1, 16 + (l >> 4));
+    const double2 abC = *reinterpret_cast<const double2*>(CF + 2 * cX);
+    const double aC = abC.x, bC = abC.y;
     const double* G = rowv + q;
     const double* DX = rowv + LD + q;
     const double* U = rowv + 2 * LD + q;
@@ -483,7 +515,7 @@ struct WideStart {
       }
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {  // the C rows: 16 consecutive rows per load
+    for (int t = 0; t < XT; ++t) {  // the extra column's rows: 16 consecutive rows per load
       const int r = rC0 + 16 * t;
       h1[3 * RR + t] = fma(rowv[LD + r], aC, fma(rowv[2 * LD + r], bC, h1[3 * RR + t]));
       wc[t & 1] = fma(h1[3 * RR + t], rowv[r], wc[t & 1]);
@@ -495,7 +527,7 @@ struct WideStart {
     constexpr int NR = ZEUS_WIDE_B3_NR;  // TMEM rows per wait (3 NR elements)
     static_assert(NT3 % NR == 0, "whole TMEM groups");
 #pragma unroll
-    for (int r0 = RR; r0 < 25; r0 += NR) {
+    for (int r0 = RR; r0 < NRW; r0 += NR) {
       double gr[NR], xr[NR], ur[NR];
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
@@ -529,10 +561,10 @@ struct WideStart {
     double c = wc[0] + wc[1];
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) c += shfl_xor(c, o);
-    if (rC0 == 0) wv[48 + (l >> 4)] = c;
-    __syncwarp();
-    w0 = wv[l];
-    w1 = l < 18 ? wv[32 + l] : 0.0;
+    if (rC0 == 0) wv[cX] = c;
+    team_sync();
+    w0 = wv[c0];
+    w1 = own1 ? wv[c1] : 0.0;
   }
 
   __device__ void run(const BfgsArgs& A, long long s, int l) {
@@ -560,9 +592,10 @@ struct WideStart {
 
     // ---- H = I, x = x0, rowv = 0
     if constexpr (BLK3) {
-      const int q = l >> 4, pq = l & 15, cC = 48 + (l >> 4), rC0 = l & 15;
+      const int L = 32 * wi + l;
+      const int q = (l >> 4) & 1, pq = 16 * wi + (l & 15), cC = 48 * W + (L >> 4), rC0 = L & 15;
 #pragma unroll
-      for (int r = 0; r < 25; ++r) {
+      for (int r = 0; r < NRW; ++r) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           const double e = 2 * r + q == 3 * pq + k ? 1.0 : 0.0;
@@ -574,7 +607,7 @@ struct WideStart {
         }
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) h1[3 * RR + t] = rC0 + 16 * t == cC ? 1.0 : 0.0;
+      for (int t = 0; t < XT; ++t) h1[3 * RR + t] = rC0 + 16 * t == cC ? 1.0 : 0.0;
       rowv[4 * LD + 2 * c0] = 0.0;  // column coefficients (a, b) by column
       rowv[4 * LD + 2 * c0 + 1] = 0.0;
       rowv[4 * LD + 2 * c1] = 0.0;
@@ -786,7 +819,7 @@ struct WideStart {
         double wa[4] = {0.0, 0.0, 0.0, 0.0}, wb[4] = {0.0, 0.0, 0.0, 0.0};
         static_assert(BLK3 || RR % 2 == 0, "register rows in pairs");
         if constexpr (BLK3) {
-          hpass_blk3(l, h1, a1, b1, w0, w1);
+          hpass_blk3(l, h1, c0, c1, own1, w0, w1);
         } else {
 #pragma unroll
         for (int i = 0; i < RR; i += 2) {
@@ -953,7 +986,7 @@ struct WideStart {
 
 template <class Obj, int RR, int W, int D, bool TM>
 __global__ void __launch_bounds__(TM ? 32 * kTmWarps : kWideThreads,
-                                  TM ? WideShape<Obj, 1>::TM_CTAS
+                                  TM ? WideShape<Obj, W>::TM_CTAS
                                      : (W == 1 && D > 0 && D <= 32) ? WideShape<Obj, 1>::SEQ_MINB
                                                                     : WideShape<Obj, W>::MINB)
     bfgs_wide_kernel(BfgsArgs A) {
@@ -969,7 +1002,7 @@ __global__ void __launch_bounds__(TM ? 32 * kTmWarps : kWideThreads,
     }
   }
   if constexpr (TM) {
-    if (wib == 0) tmem::alloc(&tm_slot, kTmAlloc);
+    if (wib == 0) tmem::alloc(&tm_slot, WideShape<Obj, W>::TM_COLS);
     tmem::fence_before_sync();
   }
   __syncthreads();
@@ -984,18 +1017,20 @@ __global__ void __launch_bounds__(TM ? 32 * kTmWarps : kWideThreads,
   S.atab = alpha_tab;
   S.rowv = sm + A.nalpha + (size_t)start_slot * A.warp_doubles;
   S.Hs = S.rowv + 4 * 64 * W;
-  S.xch = S.Hs + (size_t)(A.d > RR && !TM ? A.d - RR : 0) * 64 * W;
-  __shared__ long long next;
+  // TM: rowv, the (a, b) by column and then the exchange scratch
+  S.xch = TM ? S.rowv + 6 * 64 * W : S.Hs + (size_t)(A.d > RR ? A.d - RR : 0) * 64 * W;
+  S.bar_id = 1 + start_slot;  // (used when several multi-warp starts share the CTA)
+  __shared__ long long next[kTmWarps];
   for (;;) {
     long long s = 0;
     if constexpr (W == 1) {
       if (l == 0) s = (long long)atomicAdd(A.work, 1ull);
       s = __shfl_sync(kFull, s, 0);
     } else {
-      if (threadIdx.x == 0) next = (long long)atomicAdd(A.work, 1ull);
-      __syncthreads();
-      s = next;
-      __syncthreads();
+      if (S.wi == 0 && l == 0) next[start_slot] = (long long)atomicAdd(A.work, 1ull);
+      S.team_sync();
+      s = next[start_slot];
+      S.team_sync();
     }
     if (s >= A.n) break;
     S.run(A, s, l);
@@ -1004,7 +1039,7 @@ __global__ void __launch_bounds__(TM ? 32 * kTmWarps : kWideThreads,
     tmem::wait_st();
     tmem::fence_before_sync();
     __syncthreads();
-    if (wib == 0) tmem::dealloc(tm_slot, kTmAlloc);
+    if (wib == 0) tmem::dealloc(tm_slot, WideShape<Obj, W>::TM_COLS);
   }
 }
 
@@ -1016,7 +1051,9 @@ int launch_wide(BfgsArgs A, cudaStream_t s) {
   const int threads = TM ? 32 * kTmWarps : kWideThreads;
   // per start: rowv only (TM: the H rows are in Tensor Memory), else the full slice
   // (d <= 32: 64 more doubles, the SEQ folds' second scratch row)
-  A.warp_doubles = TM ? 6 * 64 : wide_slot_doubles(A.d, RR, W) + (A.d <= 32 ? 64 : 0);
+  // TM: rowv [4][64 W] + (a, b) by column [64 W][2] + the W > 1 exchange scratch
+  A.warp_doubles = TM ? ((6 * 64 * W + (W > 1 ? 19 * W : 0) + 1) & ~1)
+                      : wide_slot_doubles(A.d, RR, W) + (A.d <= 32 ? 64 : 0);
   const int starts_per_block = threads / 32 / W;
   const size_t smem =
       sizeof(double) * ((size_t)A.nalpha + (size_t)starts_per_block * A.warp_doubles);
@@ -1031,7 +1068,7 @@ int launch_wide(BfgsArgs A, cudaStream_t s) {
   if (rc) return rc;
   // TM: the CTAs per SM whose TMEM allocations fit the SM's 512 columns (the
   // occupancy API reports 1 for kernels that allocate TMEM)
-  if (TM) per_sm = WideShape<Obj, 1>::TM_CTAS;
+  if (TM) per_sm = WideShape<Obj, W>::TM_CTAS;
   const int sms = current_sm_count();
   if (per_sm < 1 || sms < 1) return set_error(ZEUS_ERR_UNSUPPORTED, "bfgs wide: does not fit");
   int64_t grid = (int64_t)per_sm * sms;
@@ -1066,6 +1103,9 @@ struct WideLaunch {
         if (A.d == 20) return launch_wide<Obj, 20, 1, 20>(A, s);
       if (A.d == 50) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 50>(A, s);
       if (A.d <= 64) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 0>(A, s);
+#ifndef ZEUS_WIDE_NO_TMEM
+      if (A.d == 100) return launch_wide<Obj, WideShape<Obj, 2>::RR_TM, 2, 100, true>(A, s);
+#endif
       if (A.d == 100) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2, 100>(A, s);
       return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2, 0>(A, s);
     }

@@ -78,6 +78,19 @@ struct WideTraits {
 };
 
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(kFull, v, src); }
+
+// f from the folded accumulators / gradient component from term tangents;
+// Ackley's out-of-line copies (objectives.cuh) keep the kernels' code small
+template <class Obj>
+__device__ __forceinline__ double wfinish(const double* acc, int d, bool& err) {
+  if constexpr (Obj::kId == ZEUS_OBJ_ACKLEY) return Obj::finish_ool(acc, d, err);
+  else return Obj::finish(acc, d, err);
+}
+template <class Obj, class TA>
+__device__ __forceinline__ double wgrad(const TA& tan, int i, int d, const double* acc, bool& err) {
+  if constexpr (Obj::kId == ZEUS_OBJ_ACKLEY) return Obj::grad_from_tan_ool(tan, i, d, acc, err);
+  else return Obj::grad_from_tan(tan, i, d, acc, err);
+}
 __device__ __forceinline__ double shfl_xor(double v, int m) { return __shfl_xor_sync(kFull, v, m); }
 
 }  // namespace
@@ -451,9 +464,9 @@ struct WideStart {
       }
     }
     g0 = 0.0;
-    if ((W == 1 && D > 32) || c0 < d) g0 = Obj::grad_from_tan(LT{c0, tA[0], tA[1], prevA}, c0, d, acc, err);
+    if ((W == 1 && D > 32) || c0 < d) g0 = wgrad<Obj>(LT{c0, tA[0], tA[1], prevA}, c0, d, acc, err);
     g1 = 0.0;
-    if (c1 < d) g1 = Obj::grad_from_tan(LT{c1, tB[0], tB[1], prevB}, c1, d, acc, err);
+    if (c1 < d) g1 = wgrad<Obj>(LT{c1, tB[0], tB[1], prevB}, c1, d, acc, err);
   }
 
   // neighbour coordinates (Rosenbrock term j needs x_{j+1}) of two lane
@@ -657,7 +670,7 @@ struct WideStart {
         for (int a = 0; a < NA; ++a) acc[a] = Obj::init(a, d) + team_sum(sv[a], l);
       }
       bool ferr = false;
-      f0 = Obj::finish(acc, d, ferr);
+      f0 = wfinish<Obj>(acc, d, ferr);
       if (A.stop_flag && team_any(*(volatile int*)A.stop_flag != 0)) {
         status = ZEUS_STOPPED;
         goto done;
@@ -752,9 +765,9 @@ struct WideStart {
             bool ferr = false;
             if constexpr (NA > 1) {  // Ackley: exp / sqrt only for trials that exist
               fb[c] = 0.0;
-              if (valid) fb[c] = Obj::finish(ab, d, ferr);
+              if (valid) fb[c] = wfinish<Obj>(ab, d, ferr);
             } else {
-              fb[c] = Obj::finish(ab, d, ferr);
+              fb[c] = wfinish<Obj>(ab, d, ferr);
             }
             // NaN fails; the trial at t = iter_ls is taken when nothing passed
             const bool pass = fb[c] <= f0 + A.c1 * al[c] * ddir || t0 + c == A.iter_ls;

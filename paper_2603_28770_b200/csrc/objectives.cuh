@@ -243,6 +243,20 @@ struct Ackley {
     return -20.0 * gexp(-0.2 * gsqrt(sum_sq / (double)d, err), err) -
            gexp(sum_cos / (double)d, err) + kE + 20.0;
   }
+  // Out-of-line copies for the one-warp-per-start kernels (bfgs_wide.cu): one
+  // copy of the exp / sqrt chains in the instruction cache instead of one
+  // per call site -- the inlined d = 50 kernel stalled on instruction fetch
+  // (ncu no_instruction 2.7 warps per issue): 1,091 -> 1,026 SM-cycles per
+  // start-iteration at d = 50, 3,903 -> 3,744 at d = 100, same results.  The
+  // small-d kernels keep the inline form (4-7% faster there).
+  __device__ __noinline__ static double finish_ool(const double acc[2], int d, bool& err) {
+    return outer<double>(acc[0], acc[1], d, err);
+  }
+  template <class TA>
+  __device__ __noinline__ static double grad_from_tan_ool(const TA& tan, int i, int d,
+                                                          const double* acc, bool& err) {
+    return outer<Dual>(Dual{acc[0], tan(i, 0)}, Dual{acc[1], tan(i, 1)}, d, err).d;
+  }
   __device__ static double finish(const double acc[2], int d, bool& err) {
     return outer<double>(acc[0], acc[1], d, err);
   }

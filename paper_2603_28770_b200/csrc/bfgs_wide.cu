@@ -42,6 +42,8 @@
 //  5. g'.p' (the next line search's ddir) by one butterfly.
 // Objective folds for d > 16 are trees: f agrees with
 // the reference's sequential fold to ~1 ulp, inside the stated tolerance.
+#include <cstdlib>
+
 #include "bfgs_common.cuh"
 #include "tmem.cuh"
 
@@ -1110,14 +1112,18 @@ struct WideLaunch {
       // start-iteration, TMEM block layout / shared-memory rows: Rosenbrock
       // 448 / 628, Rastrigin 1,062 / 1,251, Ackley 1,120 / 1,341)
 #ifndef ZEUS_WIDE_NO_TMEM
-      if (A.d == 50) return launch_wide<Obj, WideShape<Obj, 1>::RR_TM, 1, 50, true>(A, s);
+      // (ZEUS_NO_TMEM=1: the shared-memory kernels, for compute-sanitizer's
+      // synccheck, which flags every tcgen05.alloc -- csrc/tools/tmem_synccheck.cu)
+      const char* no_tm = getenv("ZEUS_NO_TMEM");
+      const bool tmem_ok = !(no_tm && no_tm[0] && no_tm[0] != '0');
+      if (A.d == 50 && tmem_ok) return launch_wide<Obj, WideShape<Obj, 1>::RR_TM, 1, 50, true>(A, s);
 #endif
       if constexpr (Obj::kId != ZEUS_OBJ_ACKLEY)  // config 5 (Ackley: the warp kernel)
         if (A.d == 20) return launch_wide<Obj, 20, 1, 20>(A, s);
       if (A.d == 50) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 50>(A, s);
       if (A.d <= 64) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 1), 1, 0>(A, s);
 #ifndef ZEUS_WIDE_NO_TMEM
-      if (A.d == 100) return launch_wide<Obj, WideShape<Obj, 2>::RR_TM, 2, 100, true>(A, s);
+      if (A.d == 100 && tmem_ok) return launch_wide<Obj, WideShape<Obj, 2>::RR_TM, 2, 100, true>(A, s);
 #endif
       if (A.d == 100) return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2, 100>(A, s);
       return launch_wide<Obj, ZEUS_WIDE_RR_OF(Obj, 2), 2, 0>(A, s);

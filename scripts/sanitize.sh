@@ -1,8 +1,9 @@
 #!/bin/bash
 # memcheck + racecheck + synccheck of every kernel family on small configs
 # (race detection): thread / warp / CTA-team tiers (d <= 16, with
-# promotions), warp kernel (d = 24), wide kernel W = 1 (d = 40, 50) and W = 2
-# (d = 70, 100), fused PSO, the early-stop protocol, user plug-ins (thread and
+# promotions), warp kernel (d = 24), wide kernel W = 1 (d = 20 with the
+# reference-order folds, 40, 50 in TMEM) and W = 2 (d = 70, 100 in TMEM with
+# two starts per CTA), fused PSO, the early-stop protocol, user plug-ins (thread and
 # warp kernels), the multi-GPU PSO peer exchange (3 emulated ranks).
 mkdir -p gpurun_out
 cat > /tmp/san.py <<'PY'
@@ -12,6 +13,8 @@ for name, d, n, cap, workers in (("rastrigin", 10, 300, 120, 0), ("rosenbrock", 
                                  ("rosenbrock", 24, 8, 60, 0), ("ackley", 50, 8, 60, 0),
                                  ("rastrigin", 40, 5, 60, 0), ("rosenbrock", 100, 3, 60, 0),
                                  ("rastrigin", 70, 3, 60, 0), ("goldstein_price", 2, 33, 60, 0),
+                                 ("rastrigin", 20, 9, 60, 0), ("rosenbrock", 20, 9, 60, 0),
+                                 ("rosenbrock", 100, 5, 60, 2),
                                  ("rastrigin", 10, 200, 60, 2), ("rosenbrock", 50, 8, 60, 2)):
     spec = z.get_objective(name, d)
     cfg = z.ZeusConfig(N=n, dim=d, range=(spec.lower, spec.upper), iter_pso=2, iter_bfgs=cap,
@@ -49,8 +52,12 @@ for q, (sh, nq) in enumerate(shards):
 torch.cuda.synchronize()
 print("exchange", [float(sh.gbest[0]) for sh, _ in shards])
 PY
+# synccheck flags every tcgen05.alloc (a bare alloc/dealloc kernel included:
+# csrc/tools/tmem_synccheck.cu), so it runs on the shared-memory kernels
+# (ZEUS_NO_TMEM=1); memcheck and racecheck cover the TMEM kernels too
 for tool in memcheck racecheck synccheck; do
-  timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san.py > gpurun_out/$tool.txt 2>&1
+  env=""; [ $tool = synccheck ] && env="ZEUS_NO_TMEM=1"
+  timeout 1200 env $env compute-sanitizer --tool $tool --print-limit 20 python /tmp/san.py > gpurun_out/$tool.txt 2>&1
   echo "$tool rc=$?" >> gpurun_out/$tool.txt
   tail -6 gpurun_out/$tool.txt
 done

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define ZEUS_ABI_VERSION 1
+#define ZEUS_ABI_VERSION 2
 
 /* objective ids (objectives.py:145-182 _REGISTRY) */
 #define ZEUS_OBJ_ROSENBROCK 0
@@ -63,6 +63,16 @@ typedef struct zeus_bfgs_out {
   uint8_t *status;      /* BfgsOutcome.status (ZEUS_CONVERGED ...)        */
   int32_t *ls_trials;   /* objective evaluations spent in line searches   */
   int32_t *grad_evals;  /* forward-AD gradient evaluations                */
+  /* Optional (NULL: not written): every start's outcome also as host-ready
+   * rows, the zeus_pack_results layout -- rows[s * ld_rows + k] = x_final[k]
+   * (k < d), [d] = f_final, [d + 1] = grad_norm; irows[4 s .. 4 s + 3] =
+   * (iterations, status, ls_trials, grad_evals), 16-byte aligned.  They may
+   * be page-locked host memory (device address from zeus_host_device_ptr):
+   * each start's outcome then reaches the host as the start finishes, with
+   * no pack kernel and no copy after the run. */
+  double *rows;
+  int64_t ld_rows;
+  int32_t *irows;
 } zeus_bfgs_out;
 
 /* BFGS / line-search hyper-parameters: bfgs_run(theta, iter_bfgs) bfgs.py:80-87,
@@ -219,6 +229,9 @@ int zeus_count_within(int d, int64_t n, const double *x, int64_t ldx, const doub
 int zeus_pack_results(const zeus_bfgs_out *out, int d, int64_t n, double *fpack, int32_t *ipack,
                       const unsigned long long *tallies, const double *gbest, const double *best,
                       int nbest, double *spack, void *stream);
+/* Device address of page-locked host memory (cudaHostGetDevicePointer), for
+ * zeus_bfgs_out.rows / irows. */
+int zeus_host_device_ptr(void *host, void **dev);
 
 /* ---- cross-GPU early stop: driver.py:137-202 (_init_worker / _run_parallel's
  * shared Value('q') counter and Value('i') flag, one per pool).  Here the pool

@@ -21,7 +21,7 @@ OBJ_RASTRIGIN = 1
 OBJ_ACKLEY = 2
 OBJ_GOLDSTEIN_PRICE = 3
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _i32, _i64, _u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
 _int, _dbl, _vp, _sz = ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
@@ -39,7 +39,7 @@ class BfgsParams(ctypes.Structure):
 class BfgsOut(ctypes.Structure):
     _fields_ = [("x_final", _vp), ("ld_out", _i64), ("f_final", _vp), ("grad_norm", _vp),
                 ("iterations", _vp), ("status", _vp), ("ls_trials", _vp),
-                ("grad_evals", _vp)]
+                ("grad_evals", _vp), ("rows", _vp), ("ld_rows", _i64), ("irows", _vp)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/zeus_b200.h
@@ -77,6 +77,7 @@ _SIGNATURES = {
     "zeus_count_within": (_int, [_int, _i64, _vp, _i64, _vp, _dbl, _vp, _vp]),
     "zeus_pack_results": (_int, [ctypes.POINTER(BfgsOut), _int, _i64, _vp, _vp, _vp, _vp, _vp,
                                  _int, _vp, _vp]),
+    "zeus_host_device_ptr": (_int, [_vp, ctypes.POINTER(_vp)]),
     "zeus_user_compile": (_int, [ctypes.c_char_p, _int, ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "zeus_user_compile_log": (ctypes.c_char_p, []),
     "zeus_user_free": (_int, [_vp]),

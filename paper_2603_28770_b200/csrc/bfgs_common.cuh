@@ -108,6 +108,18 @@ constexpr int kMaxC = 32;       // columns per lane in the smem / HBM path: d <=
 __host__ __device__ inline size_t hsize(int d, int ldh) { return ((size_t)d * ldh + 1) & ~(size_t)1; }
 
 
+// The optional host-ready row of start s (zeus_bfgs_out.rows / irows): its
+// scalar tail (x is written by the coordinate owners next to x_final).
+__device__ __forceinline__ void write_row_tail(const zeus_bfgs_out& o, long long s, int d,
+                                               double f, double gn, int k, int status,
+                                               int ls_trials, int grads) {
+  if (!o.rows) return;
+  double* r = o.rows + s * o.ld_rows;
+  r[d] = f;
+  r[d + 1] = gn;
+  *reinterpret_cast<int4*>(o.irows + 4 * s) = make_int4(k, status, ls_trials, grads);
+}
+
 // Trial-point accessor: coordinate j of x + alpha p (reference: x + alpha*p,
 // numpy multiply then add, no contraction).
 struct TrialX {

@@ -309,6 +309,12 @@ struct ThreadStart {
 #pragma unroll
     for (int j = 0; j < D; ++j)
       if (j < d) o.x_final[(int64_t)j * o.ld_out + s] = x[j];
+    if (o.rows) {
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+        if (j < d) o.rows[(int64_t)s * o.ld_rows + j] = x[j];
+    }
+    write_row_tail(o, s, d, f0, sqrt(gsq), k, status, ls_trials, grads);
     o.f_final[s] = f0;
     o.grad_norm[s] = sqrt(gsq);
     o.iterations[s] = k;

@@ -522,7 +522,10 @@ struct BfgsWarp {
   done:
     const zeus_bfgs_out& o = A.out;
     for (int j = lane; j < d; j += 32) o.x_final[(int64_t)j * o.ld_out + s] = x[j];
+    if (o.rows)
+      for (int j = lane; j < d; j += 32) o.rows[(int64_t)s * o.ld_rows + j] = x[j];
     if (lane == 0) {
+      write_row_tail(o, s, d, f0, sqrt(gsq), k, status, ls_trials, grads);
       o.f_final[s] = f0;
       o.grad_norm[s] = sqrt(gsq);
       o.iterations[s] = k;

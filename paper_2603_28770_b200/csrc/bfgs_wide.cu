@@ -983,7 +983,12 @@ struct WideStart {
     const zeus_bfgs_out& o = A.out;
     if (own0) o.x_final[(int64_t)c0 * o.ld_out + s] = x0;
     if (own1) o.x_final[(int64_t)c1 * o.ld_out + s] = x1;
+    if (o.rows) {
+      if (own0) o.rows[(int64_t)s * o.ld_rows + c0] = x0;
+      if (own1) o.rows[(int64_t)s * o.ld_rows + c1] = x1;
+    }
     if (wi == 0 && l == 0) {
+      write_row_tail(o, s, d, f0, sqrt(gsq), k, status, ls_trials, grads);
       o.f_final[s] = f0;
       o.grad_norm[s] = sqrt(gsq);
       o.iterations[s] = k;

@@ -360,6 +360,11 @@ int zeus_pack_results(const zeus_bfgs_out* out, int d, int64_t n, double* fpack,
   return check_launch("pack_results_kernel");
 }
 
+int zeus_host_device_ptr(void* host, void** dev) {
+  if (!host || !dev) return set_error(ZEUS_ERR_ARGUMENT, "zeus_host_device_ptr");
+  return check_cuda(cudaHostGetDevicePointer(dev, host, 0), "cudaHostGetDevicePointer");
+}
+
 // ---- cross-process early-stop block (driver.py:153-177 across GPUs) --------
 // 64 bytes of cudaMalloc'ed device memory: counter (u64) at 0, flag (i32) at 8.
 // Its own allocation, so the IPC handle maps exactly this block (torch's

@@ -64,15 +64,22 @@ class BfgsBuffers:
             grad_evals=torch.empty(max(n, 1), dtype=torch.int32, device=device),
         )
 
+    # optional host-ready rows (zeus_bfgs_out.rows / irows): device addresses
+    # of [n][ld_rows] f64 and [n][4] i32 tables, set by zeus_run
+    rows: Optional[tuple] = None
+
     def c_struct(self, n: int, lo: int = 0) -> _capi.BfgsOut:
         """The C view of starts [lo, lo + n) (same row stride)."""
+        rows_ptr, ld_rows, irows_ptr = self.rows or (None, 0, None)
         return _capi.BfgsOut(
             x_final=self.x_final.data_ptr() + 8 * lo, ld_out=self.x_final.shape[1],
             f_final=self.f_final.data_ptr() + 8 * lo,
             grad_norm=self.grad_norm.data_ptr() + 8 * lo,
             iterations=self.iterations.data_ptr() + 4 * lo, status=self.status.data_ptr() + lo,
             ls_trials=self.ls_trials.data_ptr() + 4 * lo,
-            grad_evals=self.grad_evals.data_ptr() + 4 * lo)
+            grad_evals=self.grad_evals.data_ptr() + 4 * lo,
+            rows=rows_ptr + 8 * lo * ld_rows if rows_ptr else None, ld_rows=ld_rows,
+            irows=irows_ptr + 16 * lo if irows_ptr else None)
 
 
 def bfgs_params(theta: float, iter_bfgs: int, ls) -> _capi.BfgsParams:

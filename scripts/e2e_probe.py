@@ -15,7 +15,8 @@ obj, d, n, sweeps, cap, box = CFG[name]
 fn = getattr(z, obj)
 cfg = lambda s: z.ZeusConfig(N=n, dim=d, range=box, iter_pso=sweeps, iter_bfgs=cap, seed=s,
                              deterministic=True)
-for s in range(3): z.zeus_run(fn, cfg(1000 + s))
+r = None
+for s in range(3): r = z.zeus_run(fn, cfg(1000 + s))  # (held: the result-table pool's steady state)
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 rows = []
 for s in range(6):

@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert hasattr(L, name), name
     assert sorted(_capi.EXPORTED_SYMBOLS) == declared
-    assert L.zeus_abi_version() == 1
+    assert L.zeus_abi_version() == _capi.ABI_VERSION == 2
     assert L.zeus_pso_workspace_bytes(1000) >= 16
 
 

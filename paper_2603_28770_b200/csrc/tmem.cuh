@@ -13,7 +13,8 @@
 // registers into and out of the 16-register operand blocks (~200 moves per
 // BFGS iteration, measured), a hand-written asm chunk fared worse, and .x4
 // (one row's two columns per access) traded the 64 saved accesses for ~100
-// register moves around the 4-register operands (Rosenbrock d = 50 +2%).
+// register moves around the 4-register operands (Rosenbrock d = 50 +2%); in the block
+// layout one .x8 + one .x4 access per two-row group measured +4% too.
 #pragma once
 #include <cstdint>
 

@@ -480,7 +480,10 @@ def main():
                 "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(sum(recs[0][j]["d2h"] for j in range(NP))),
                 "path": "zeus_run(f, ZeusConfig(...)) wall time per problem, every start's "
-                        "outcome (x_final, f, |g|, k, status, counters) copied to host",
+                        "outcome (x_final, f, |g|, k, status, counters) delivered to host "
+                        "memory (one GPU: written by the BFGS kernels into page-locked, "
+                        "device-mapped host rows as each start finishes; several ranks: "
+                        "packed, gathered and copied D2H); d2h_bytes_per_step = those rows",
                 "inputs": "the call's inputs are (objective, config, seed): kernel arguments "
                           "only; the swarm is generated on the device by the reference's "
                           "Philox stream (SURVEY S1), so no input bytes cross PCIe"},

@@ -77,6 +77,11 @@ struct LT {
 template <class Obj>
 struct WideTraits {
   static constexpr bool kNeighbour = Obj::kId == ZEUS_OBJ_ROSENBROCK;
+  // the objective evaluates trig (a fast-path range fallback is possible) /
+  // can raise a DomainError (Ackley's sqrt'(0), autodiff.py:207-213); without
+  // them the team votes on oor / err are skipped (a barrier each at W = 2)
+  static constexpr bool kTrig = Obj::kId == ZEUS_OBJ_RASTRIGIN || Obj::kId == ZEUS_OBJ_ACKLEY;
+  static constexpr bool kErr = Obj::kId == ZEUS_OBJ_ACKLEY;
 };
 
 __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(kFull, v, src); }
@@ -655,7 +660,8 @@ struct WideStart {
       double sv[NA], tA[2], tB[2];
       bool oor = false, err = false;
       lane_tan<FastMath>(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB, oor);
-      if (team_any(oor)) lane_tan_precise(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB);
+      if (WideTraits<Obj>::kTrig && team_any(oor))
+        lane_tan_precise(d, nt, c0, x0, x1, nx0, nx1, sv, tA, tB);
 #pragma unroll
       if constexpr (SEQ) {
         double v[8], in[8];
@@ -679,7 +685,7 @@ struct WideStart {
       }
       ++grads;
       lane_grad(d, l, c0, tA, tB, acc, g0, g1, err);
-      if (team_any(err)) {
+      if (WideTraits<Obj>::kErr && team_any(err)) {
         status = ZEUS_DOMAIN_ERROR;
         goto done;
       }
@@ -727,7 +733,7 @@ struct WideStart {
           }
           bool oor = false;
           lane_terms<FastMath, CH>(d, nt, c0, al, x0, x1, p0, p1, nx0, nx1, np0, np1, sc, oor);
-          if (team_any(oor))  // some |2 pi x| > kTrigMax: CUDA libm, out of line
+          if (WideTraits<Obj>::kTrig && team_any(oor))  // some |2 pi x| > kTrigMax: libm
             lane_terms_precise<CH>(d, nt, c0, al, x0, x1, p0, p1, nx0, nx1, np0, np1,
                                    &sc[0][0]);
           double v[8];
@@ -808,9 +814,10 @@ struct WideStart {
         double sv[NA], tA[2], tB[2];
         bool oor = false, err = false;
         lane_tan<FastMath>(d, nt, c0, xn0, xn1, nxn0, nxn1, sv, tA, tB, oor);
-        if (team_any(oor)) lane_tan_precise(d, nt, c0, xn0, xn1, nxn0, nxn1, sv, tA, tB);
+        if (WideTraits<Obj>::kTrig && team_any(oor))
+          lane_tan_precise(d, nt, c0, xn0, xn1, nxn0, nxn1, sv, tA, tB);
         lane_grad(d, l, c0, tA, tB, acc_new, gn0, gn1, err);
-        if (team_any(err)) {
+        if (WideTraits<Obj>::kErr && team_any(err)) {
           status = ZEUS_DOMAIN_ERROR;
           break;
         }

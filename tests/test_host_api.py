@@ -181,3 +181,63 @@ def test_no_cpu_fallback_without_gpu(z):
         z.zeus_run(z.rosenbrock, cfg)
     with pytest.raises(ZeusNativeError):
         z.rosenbrock([1.0, 1.0])
+
+
+def test_abi_structs_match_the_header(tmp_path):
+    """The ctypes mirrors of zeus_bfgs_out / zeus_bfgs_params have the C
+    layout of include/zeus_b200.h (size and every field offset, compiled
+    with the host C compiler): a drift would hand the kernels garbage
+    pointers."""
+    import ctypes
+    import subprocess
+
+    from paper_2603_28770_b200 import _capi
+
+    fields = {"zeus_bfgs_out": [f for f, _ in _capi.BfgsOut._fields_],
+              "zeus_bfgs_params": [f for f, _ in _capi.BfgsParams._fields_]}
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "zeus_b200.h"', 'int main(void) {']
+    for st, fs in fields.items():
+        src.append(f'  printf("{st} %zu\\n", sizeof({st}));')
+        src += [f'  printf("{st}.{f} %zu\\n", offsetof({st}, {f}));' for f in fs]
+    src.append("  return 0;\n}")
+    c = tmp_path / "abi.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)],
+                   check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True,
+                                                       text=True, check=True).stdout.splitlines())
+    for st, cls in (("zeus_bfgs_out", _capi.BfgsOut), ("zeus_bfgs_params", _capi.BfgsParams)):
+        assert int(got[st]) == ctypes.sizeof(cls), st
+        for f in fields[st]:
+            assert int(got[f"{st}.{f}"]) == getattr(cls, f).offset, (st, f)
+
+
+def test_early_stop_waves_cover_every_start(monkeypatch):
+    """run_bfgs in the parallel early-stop mode (driver.py:153-202 pool
+    semantics): launches of wave, 2 wave, 4 wave, ... starts, contiguous and
+    covering [0, n) exactly once."""
+    import torch
+
+    from paper_2603_28770_b200 import engine
+
+    calls = []
+    monkeypatch.setattr(engine, "_run_bfgs_slice",
+                        lambda obj, x0, params, out, device, rc, stop, ws, lo, m:
+                        calls.append((lo, m)))
+    monkeypatch.setattr(engine._device, "workspace", lambda nbytes, dev: None)
+
+    class _L:
+        @staticmethod
+        def zeus_bfgs_workspace_bytes(d, n):
+            return 0
+
+    monkeypatch.setattr(engine._capi, "lib", lambda: _L)
+    x0 = torch.zeros((3, 1000), dtype=torch.float64)
+    engine.run_bfgs(0, x0, None, None, "cpu", required_c=5, stop=(0, 0), wave=7)
+    assert [m for _, m in calls] == [7, 14, 28, 56, 112, 224, 448, 111]
+    assert calls[0][0] == 0 and all(a + m == b for (a, m), (b, _) in zip(calls, calls[1:]))
+    assert sum(m for _, m in calls) == 1000
+    calls.clear()
+    engine.run_bfgs(0, x0, None, None, "cpu", required_c=5, stop=None, wave=7)
+    assert calls == [(0, 1000)]  # no stop block: one launch

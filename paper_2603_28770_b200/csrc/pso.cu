@@ -5,6 +5,44 @@
 
 namespace zeus {
 
+// Block partials a shard's workspace holds: enough for the tiled sweep's
+// smallest tile (16 particles per CTA) and for the one-thread-per-particle
+// kernels (kPsoBlock per CTA).
+static int64_t pso_partials_max(int64_t n) {
+  const int64_t nb = (n + 15) / 16;
+  return nb < 1 ? 1 : nb;
+}
+
+// One sweep launch: the tiled kernel for d <= kStreamMax (every registered
+// objective's sweep), else one thread per particle.  Returns the grid size
+// (= the number of block partials written).
+template <class Obj>
+static int launch_sweep(int d, int64_t n, int64_t i0, uint64_t seed, uint64_t k0, double w,
+                        double c1, double c2, double* x, double* v, double* p, double* pval,
+                        int64_t ld, const double* gX, double* blk_f, long long* blk_i,
+                        unsigned* done, double* cand, double* gX_out, double* gbest_out,
+                        const PsoXchg* xg, unsigned long long seq, cudaStream_t s) {
+  if (d <= kStreamMax) {
+    static const bool attr = [] {
+      return cudaFuncSetAttribute(pso_sweep_tiled_kernel<Obj>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  64 * 1024) == cudaSuccess;
+    }();
+    (void)attr;
+    const int P = 1 << pso_tile_log2(d);
+    const int nb = n > 0 ? (int)((n + P - 1) / P) : 1;
+    pso_sweep_tiled_kernel<Obj><<<nb, kPsoBlock, pso_tile_smem(d), s>>>(
+        d, n, i0, seed, k0, w, c1, c2, x, v, p, pval, ld, gX, blk_f, blk_i, done, cand, gX_out,
+        gbest_out, xg, seq);
+    return nb;
+  }
+  const int nb = n > 0 ? (int)((n + kPsoBlock - 1) / kPsoBlock) : 1;
+  pso_sweep_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, k0, w, c1, c2, x, v, p, pval,
+                                                 ld, gX, blk_f, blk_i, done, cand, gX_out,
+                                                 gbest_out, xg, seq);
+  return nb;
+}
+
 struct PsoInitLaunch {
   template <class Obj>
   static int run(int d, int64_t n, int64_t i0, uint64_t seed, double lower, double upper,
@@ -12,7 +50,7 @@ struct PsoInitLaunch {
                  void* ws, cudaStream_t s) {
     const int nb = (int)((n + kPsoBlock - 1) / kPsoBlock);
     double* blk_f = (double*)ws;
-    long long* blk_i = (long long*)(blk_f + nb);
+    long long* blk_i = (long long*)(blk_f + pso_partials_max(n));
     const double range = upper - lower;
     const double vr = upper - lower;  // vel_range (pso.py:101)
     const double vlow = -vr, vrange = vr - (-vr);
@@ -31,13 +69,11 @@ struct PsoSweepLaunch {
   static int run(int d, int64_t n, int64_t i0, uint64_t seed, int sweep, double w, double c1,
                  double c2, double* x, double* v, double* p, double* pval, int64_t ld,
                  const double* gX, double* cand, void* ws, cudaStream_t s) {
-    const int nb = (int)((n + kPsoBlock - 1) / kPsoBlock);
     double* blk_f = (double*)ws;
-    long long* blk_i = (long long*)(blk_f + nb);
+    long long* blk_i = (long long*)(blk_f + pso_partials_max(n));
     const uint64_t k0 = (uint64_t)(2 * d) * (uint64_t)(sweep + 1);
-    pso_sweep_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, k0, w, c1, c2, x, v, p,
-                                                   pval, ld, gX, blk_f, blk_i, nullptr, nullptr,
-                                                   nullptr, nullptr, nullptr, 0ull);
+    const int nb = launch_sweep<Obj>(d, n, i0, seed, k0, w, c1, c2, x, v, p, pval, ld, gX, blk_f,
+                                     blk_i, nullptr, nullptr, nullptr, nullptr, nullptr, 0ull, s);
     int rc = check_launch("pso_sweep_kernel");
     if (rc) return rc;
     pso_finalize_kernel<<<1, kPsoBlock, 0, s>>>(d, nb, i0, p, ld, blk_f, blk_i, cand);
@@ -60,8 +96,8 @@ struct PsoRunLaunch {
                  const PsoXchg* xg, unsigned long long seq0, cudaStream_t s) {
     const int nb = n > 0 ? (int)((n + kPsoBlock - 1) / kPsoBlock) : 1;
     double* blk_f = (double*)ws;
-    long long* blk_i = (long long*)(blk_f + nb);
-    unsigned* done = (unsigned*)(blk_i + nb);
+    long long* blk_i = (long long*)(blk_f + pso_partials_max(n));
+    unsigned* done = (unsigned*)(blk_i + pso_partials_max(n));
     int rc = check_cuda(cudaMemsetAsync(done, 0, sizeof(unsigned), s), "memset(pso done)");
     if (rc) return rc;
     const double range = upper - lower, vr = upper - lower;  // pso.py:101
@@ -71,9 +107,8 @@ struct PsoRunLaunch {
     rc = check_launch("pso_init_kernel(fused)");
     for (int sw = 0; sw < iter_pso && !rc; ++sw) {
       const uint64_t k0 = (uint64_t)(2 * d) * (uint64_t)(sw + 1);
-      pso_sweep_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, k0, w, c1, c2, x, v, p,
-                                                     pval, ld, gX, blk_f, blk_i, done, cand, gX,
-                                                     gbest, xg, seq0 + 1 + (unsigned)sw);
+      launch_sweep<Obj>(d, n, i0, seed, k0, w, c1, c2, x, v, p, pval, ld, gX, blk_f, blk_i,
+                        done, cand, gX, gbest, xg, seq0 + 1 + (unsigned)sw, s);
       rc = check_launch("pso_sweep_kernel(fused)");
     }
     return rc;
@@ -96,9 +131,9 @@ using namespace zeus;
 extern "C" {
 
 size_t zeus_pso_workspace_bytes(int64_t n) {
-  const int64_t nb = (n + kPsoBlock - 1) / kPsoBlock;
-  // block partials + the fused barrier's ticket counter (zeus_pso_run)
-  return (size_t)(nb < 1 ? 1 : nb) * (sizeof(double) + sizeof(long long)) + 16;
+  // block partials (as many as the tiled sweep's smallest tile leaves) +
+  // the fused barrier's ticket counter (zeus_pso_run)
+  return (size_t)pso_partials_max(n) * (sizeof(double) + sizeof(long long)) + 16;
 }
 
 int zeus_pso_run(int obj, int d, int64_t n, int64_t i0, uint64_t seed, double lower,

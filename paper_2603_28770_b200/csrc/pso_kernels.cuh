@@ -102,13 +102,23 @@ __device__ __forceinline__ void finalize_body(int d, int nb, int64_t i0,
   __shared__ long long win;
   double bf = 0.0;
   long long bi = -1;
-  for (int b = threadIdx.x; b < nb; b += kPsoBlock) {
-    const double fb = __ldcg(blk_f + b);
-    const long long ib = __ldcg(blk_i + b);
-    if (argmin_better(fb, ib, bf, bi)) {
-      bf = fb;
-      bi = ib;
+  // partials in batches of 8 loads in flight (the tiled sweep leaves up to
+  // n / 16 of them; this loop is the serial tail of every sweep)
+  for (int b0 = threadIdx.x; b0 < nb; b0 += 8 * kPsoBlock) {
+    double fb[8];
+    long long ib[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int b = b0 + u * kPsoBlock;
+      fb[u] = b < nb ? __ldcg(blk_f + b) : 0.0;
+      ib[u] = b < nb ? __ldcg(blk_i + b) : -1;
     }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (argmin_better(fb[u], ib[u], bf, bi)) {
+        bf = fb[u];
+        bi = ib[u];
+      }
   }
   block_argmin<kPsoBlock>(bf, bi);
   if (threadIdx.x == 0) {
@@ -319,6 +329,191 @@ __global__ void __launch_bounds__(kPsoBlock)
     }
     bf = best;
     bi = i0 + i;
+  }
+  block_argmin<kPsoBlock>(bf, bi);
+  if (threadIdx.x == 0) {
+    blk_f[blockIdx.x] = bf;
+    blk_i[blockIdx.x] = bi;
+  }
+  if (done) {
+    __syncthreads();  // block_argmin's shared scratch is reused by the finalize
+    fused_finalize(done, d, i0, p, ld, blk_f, blk_i, cand, gX_out, gbest_out, xg, seq);
+  }
+}
+
+// Tiled sweep (registered objectives, d <= kStreamMax): one CTA owns P
+// particles and spreads the sweep's independent work over all its threads
+// instead of running d coordinates one after another in one thread:
+//   1. draws: the 2d draws of sweep s are counters [k0, k0 + 2d) of each
+//      particle's stream (r1 of coordinate k = counter k0 + k, r2 = k0 + d + k);
+//      task (particle, Philox block) computes one Philox4x64-10 block, so
+//      each block is generated once (the per-particle cursors of
+//      pso_sweep_kernel generate the block straddling r1 / r2 twice);
+//   2. update: task (particle, coordinate) loads x, v, p, forms v', x' in
+//      the reference's order (the same expression as pso_sweep_kernel) and
+//      stores them -- coordinate k of P consecutive particles is one
+//      coalesced segment;
+//   3. terms: task (particle, term) evaluates the objective's term on the new
+//      coordinates (the same term functions StreamAcc calls: the libm-heavy
+//      part in parallel);
+//   4. fold: thread j adds particle j's terms in coordinate order (the
+//      reference's left fold, StreamAcc's value bit for bit), applies the
+//      strict '<' personal-best rule; improved particles' p rows are then
+//      written by all threads, coalesced.
+// Objectives without a term form (PsoTerms<Obj>::NT == 0) fold StreamAcc
+// over the new coordinates in step 4 instead.
+// Shared memory: draws [2d][P] (reused for the terms) + positions [d][P]
+// doubles + P flags.  P = 2^LP.
+__host__ __device__ __forceinline__ int pso_tile_log2(int d) {
+  return d <= 32 ? 6 : d <= 64 ? 5 : 4;
+}
+__host__ __device__ __forceinline__ size_t pso_tile_smem(int d) {
+  const int P = 1 << pso_tile_log2(d);
+  return (size_t)3 * d * P * sizeof(double) + (size_t)P * sizeof(int);
+}
+
+// Term form of the registered objectives' sequential value (value_seq):
+// NT accumulators; term(k) of the NEW coordinates xs (column j, stride P);
+// fold(t) adds them in coordinate order from the reference's initial values.
+template <class Obj>
+struct PsoTerms {
+  static constexpr int NT = 0;
+};
+template <>
+struct PsoTerms<Rastrigin> {
+  static constexpr int NT = 1;
+  static constexpr int K0 = 0;  // first coordinate with a term
+  __device__ static void term(const double* xs, int k, int P, double* t) {
+    bool oor = false;
+    t[0] = Rastrigin::term1<AutoMath, double>(xs[k * P], oor);
+  }
+  __device__ static double fold(const double* t, int d, int P) {
+    double total = 10.0 * d;
+    for (int k = 0; k < d; ++k) total = total + t[k * P];
+    return total;
+  }
+};
+template <>
+struct PsoTerms<Rosenbrock> {
+  static constexpr int NT = 1;
+  static constexpr int K0 = 1;  // term k couples x[k-1], x[k]
+  __device__ static void term(const double* xs, int k, int P, double* t) {
+    t[0] = Rosenbrock::term2<double>(xs[(k - 1) * P], xs[k * P]);
+  }
+  __device__ static double fold(const double* t, int d, int P) {
+    double total = 0.0;
+    for (int k = 1; k < d; ++k) total = total + t[k * P];
+    return total;
+  }
+};
+template <>
+struct PsoTerms<Ackley> {
+  static constexpr int NT = 2;
+  static constexpr int K0 = 0;
+  __device__ static void term(const double* xs, int k, int P, double* t) {
+    bool oor = false;
+    Ackley::terms<AutoMath, double>(xs[k * P], t[0], t[1], oor);
+  }
+  __device__ static double fold(const double* t, int d, int P) {
+    double sq = 0.0, cs = 0.0;
+    for (int k = 0; k < d; ++k) {
+      sq = sq + t[k * P];
+      cs = cs + t[(d + k) * P];
+    }
+    bool err = false;
+    return Ackley::outer<double>(sq, cs, d, err);
+  }
+};
+
+template <class Obj>
+__global__ void __launch_bounds__(kPsoBlock)
+    pso_sweep_tiled_kernel(int d, int64_t n, int64_t i0, uint64_t seed, uint64_t k0, double w,
+                           double c1, double c2, double* __restrict__ x,
+                           double* __restrict__ v, double* __restrict__ p,
+                           double* __restrict__ pval, int64_t ld, const double* gX,
+                           double* blk_f, long long* blk_i, unsigned* done, double* cand,
+                           double* gX_out, double* gbest_out, const PsoXchg* xg,
+                           unsigned long long seq) {
+  using T = PsoTerms<Obj>;
+  extern __shared__ double pso_tile_sm[];
+  const int LP = pso_tile_log2(d), P = 1 << LP, PM = P - 1;
+  double* rs = pso_tile_sm;     // [2d][P] uniform draws, then [NT d][P] terms
+  double* xs = rs + 2 * d * P;  // [d][P] new positions
+  int* improved = (int*)(xs + d * P);
+  const int64_t base = (int64_t)blockIdx.x * P;
+  const int np = n > base ? (int)min((int64_t)P, n - base) : 0;
+  const uint64_t kend = k0 + 2 * (uint64_t)d;
+  const uint64_t b0 = k0 >> 2;
+  const int nblk = (int)(((kend - 1) >> 2) - b0 + 1);
+  for (int u = threadIdx.x; u < (nblk << LP); u += kPsoBlock) {
+    const int j = u & PM, q = u >> LP;
+    if (j < np) {
+      uint64_t o[4];
+      Philox4x64::block(b0 + q, seed, (uint64_t)(i0 + base + j), o);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const uint64_t c = ((b0 + q) << 2) + m;
+        // uniform_draw(u, 0, 1) == unit_double(u) exactly (0 + 1 * r, r >= 0)
+        if (c >= k0 && c < kend) rs[((int)(c - k0) << LP) + j] = unit_double(o[m]);
+      }
+    }
+  }
+  __syncthreads();
+  for (int u = threadIdx.x; u < (d << LP); u += kPsoBlock) {
+    const int j = u & PM, k = u >> LP;
+    if (j < np) {
+      const double r1 = rs[u], r2 = rs[(d << LP) + u];
+      const int64_t o = (int64_t)k * ld + base + j;
+      const double xk = x[o], vk = v[o], pk = p[o], gk = gX[k];
+      const double nv = w * vk + c1 * r1 * (pk - xk) + c2 * r2 * (gk - xk);
+      const double nx = xk + nv;
+      v[o] = nv;
+      x[o] = nx;
+      xs[u] = nx;
+    }
+  }
+  __syncthreads();
+  if constexpr (T::NT > 0) {
+    for (int u = threadIdx.x + (T::K0 << LP); u < (d << LP); u += kPsoBlock) {
+      const int j = u & PM, k = u >> LP;
+      if (j < np) {
+        double t[T::NT];
+        T::term(xs + j, k, P, t);
+#pragma unroll
+        for (int a = 0; a < T::NT; ++a) rs[((a * d) << LP) + u] = t[a];
+      }
+    }
+    __syncthreads();
+  }
+  double bf = 0.0;
+  long long bi = -1;
+  if (threadIdx.x < P) {
+    const int j = threadIdx.x;
+    int imp = 0;
+    if (j < np) {
+      double f;
+      if constexpr (T::NT > 0) {
+        f = T::fold(rs + j, d, P);
+      } else {
+        StreamAcc<Obj> acc = make_acc<Obj>(d);
+        for (int k = 0; k < d; ++k) acc.push(xs[(k << LP) + j]);
+        f = acc.result(d);
+      }
+      double best = pval[base + j];
+      if (f < best) {  // strict: ties keep the old personal best (pso.py:161)
+        best = f;
+        pval[base + j] = f;
+        imp = 1;
+      }
+      bf = best;
+      bi = i0 + base + j;
+    }
+    improved[j] = imp;
+  }
+  __syncthreads();
+  for (int u = threadIdx.x; u < (d << LP); u += kPsoBlock) {
+    const int j = u & PM, k = u >> LP;
+    if (improved[j]) p[(int64_t)k * ld + base + j] = xs[u];
   }
   block_argmin<kPsoBlock>(bf, bi);
   if (threadIdx.x == 0) {

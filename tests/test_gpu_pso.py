@@ -87,6 +87,12 @@ def test_swarm_matches_reference_golden(golden):
 
 
 @pytest.mark.parametrize("name,d,n,sweeps", [("rosenbrock", 10, 3000, 8),
+                                             # the tiled sweep's three tile widths
+                                             # (64 / 32 / 16 particles per CTA), ragged
+                                             # last tiles, draws straddling Philox blocks
+                                             ("rosenbrock", 7, 777, 9),
+                                             ("rosenbrock", 33, 1001, 6),
+                                             ("rosenbrock", 100, 333, 4),
                                              ("rastrigin", 10, 2048, 20),
                                              ("ackley", 5, 1000, 5)])
 def test_swarm_matches_oracle(oracle, name, d, n, sweeps):

@@ -43,20 +43,48 @@ static int launch_sweep(int d, int64_t n, int64_t i0, uint64_t seed, uint64_t k0
   return nb;
 }
 
+// init_swarm launch: the tiled kernel for d <= kStreamMax, else one thread
+// per particle.  Returns the grid size.
+template <class Obj>
+static int launch_init(int d, int64_t n, int64_t i0, uint64_t seed, double lower, double range,
+                       double vlow, double vrange, double* x, double* v, double* p,
+                       double* pval, int64_t ld, double* blk_f, long long* blk_i,
+                       unsigned* done, double* cand, double* gX_out, double* gbest_out,
+                       const PsoXchg* xg, unsigned long long seq, cudaStream_t s) {
+  if (d <= kStreamMax) {
+    static const bool attr = [] {
+      return cudaFuncSetAttribute(pso_init_tiled_kernel<Obj>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  64 * 1024) == cudaSuccess;
+    }();
+    (void)attr;
+    const int P = 1 << pso_tile_log2(d);
+    const int nb = n > 0 ? (int)((n + P - 1) / P) : 1;
+    pso_init_tiled_kernel<Obj><<<nb, kPsoBlock, pso_tile_smem(d), s>>>(
+        d, n, i0, seed, lower, range, vlow, vrange, x, v, p, pval, ld, blk_f, blk_i, done, cand,
+        gX_out, gbest_out, xg, seq);
+    return nb;
+  }
+  const int nb = n > 0 ? (int)((n + kPsoBlock - 1) / kPsoBlock) : 1;
+  pso_init_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, lower, range, vlow, vrange, x,
+                                                v, p, pval, ld, blk_f, blk_i, done, cand, gX_out,
+                                                gbest_out, xg, seq);
+  return nb;
+}
+
 struct PsoInitLaunch {
   template <class Obj>
   static int run(int d, int64_t n, int64_t i0, uint64_t seed, double lower, double upper,
                  double* x, double* v, double* p, double* pval, int64_t ld, double* cand,
                  void* ws, cudaStream_t s) {
-    const int nb = (int)((n + kPsoBlock - 1) / kPsoBlock);
     double* blk_f = (double*)ws;
     long long* blk_i = (long long*)(blk_f + pso_partials_max(n));
     const double range = upper - lower;
     const double vr = upper - lower;  // vel_range (pso.py:101)
     const double vlow = -vr, vrange = vr - (-vr);
-    pso_init_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, lower, range, vlow, vrange,
-                                                  x, v, p, pval, ld, blk_f, blk_i, nullptr,
-                                                  nullptr, nullptr, nullptr, nullptr, 0ull);
+    const int nb = launch_init<Obj>(d, n, i0, seed, lower, range, vlow, vrange, x, v, p, pval,
+                                    ld, blk_f, blk_i, nullptr, nullptr, nullptr, nullptr,
+                                    nullptr, 0ull, s);
     int rc = check_launch("pso_init_kernel");
     if (rc) return rc;
     pso_finalize_kernel<<<1, kPsoBlock, 0, s>>>(d, nb, i0, p, ld, blk_f, blk_i, cand);
@@ -94,16 +122,14 @@ struct PsoRunLaunch {
                  double w, double c1, double c2, int iter_pso, double* x, double* v, double* p,
                  double* pval, int64_t ld, double* cand, double* gX, double* gbest, void* ws,
                  const PsoXchg* xg, unsigned long long seq0, cudaStream_t s) {
-    const int nb = n > 0 ? (int)((n + kPsoBlock - 1) / kPsoBlock) : 1;
     double* blk_f = (double*)ws;
     long long* blk_i = (long long*)(blk_f + pso_partials_max(n));
     unsigned* done = (unsigned*)(blk_i + pso_partials_max(n));
     int rc = check_cuda(cudaMemsetAsync(done, 0, sizeof(unsigned), s), "memset(pso done)");
     if (rc) return rc;
     const double range = upper - lower, vr = upper - lower;  // pso.py:101
-    pso_init_kernel<Obj><<<nb, kPsoBlock, 0, s>>>(d, n, i0, seed, lower, range, -vr,
-                                                  vr - (-vr), x, v, p, pval, ld, blk_f, blk_i,
-                                                  done, cand, gX, gbest, xg, seq0);
+    launch_init<Obj>(d, n, i0, seed, lower, range, -vr, vr - (-vr), x, v, p, pval, ld, blk_f,
+                     blk_i, done, cand, gX, gbest, xg, seq0, s);
     rc = check_launch("pso_init_kernel(fused)");
     for (int sw = 0; sw < iter_pso && !rc; ++sw) {
       const uint64_t k0 = (uint64_t)(2 * d) * (uint64_t)(sw + 1);

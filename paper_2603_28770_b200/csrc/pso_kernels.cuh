@@ -2,8 +2,12 @@
 // included by pso.cu (registered objectives) and by the NVRTC program of a
 // user objective (plugin.cu), which instantiates the same kernels.
 //
-// One thread per particle; swarm arrays are SoA [d][ld] so that coordinate k
-// of consecutive particles is one coalesced 256-B transaction per warp.  The
+// Registered objectives (d <= kStreamMax) run the TILED kernels at the end of
+// this file (a CTA owns 16-64 particles and spreads draws, updates and
+// objective terms over its threads); pso_init_kernel / pso_sweep_kernel below
+// are one thread per particle (user objectives, larger d).  Swarm arrays are
+// SoA [d][ld] so that coordinate k of consecutive particles is one coalesced
+// transaction per warp.  The
 // uniform draws come straight from the counter-based Philox stream of the
 // particle's GLOBAL index (no RNG state in HBM); every update is evaluated
 // in the reference's numpy order without contraction, so the swarm is
@@ -425,15 +429,20 @@ struct PsoTerms<Ackley> {
   }
 };
 
-template <class Obj>
-__global__ void __launch_bounds__(kPsoBlock)
-    pso_sweep_tiled_kernel(int d, int64_t n, int64_t i0, uint64_t seed, uint64_t k0, double w,
-                           double c1, double c2, double* __restrict__ x,
-                           double* __restrict__ v, double* __restrict__ p,
-                           double* __restrict__ pval, int64_t ld, const double* gX,
-                           double* blk_f, long long* blk_i, unsigned* done, double* cand,
-                           double* gX_out, double* gbest_out, const PsoXchg* xg,
-                           unsigned long long seq) {
+// INIT: init_swarm in the same four passes (draws 0 .. 2d-1: x from draws
+// k, v from draws d + k, pso.py:101-109; p = x, pval = f).  Otherwise sweep
+// s (draws k0 = 2d(s+1) ..).  a0..a3: (lower, range, vlow, vrange) for INIT,
+// (w, c1, c2, -) for a sweep.
+template <class Obj, bool INIT>
+__device__ __forceinline__ void pso_tiled_body(int d, int64_t n, int64_t i0, uint64_t seed,
+                                               uint64_t k0, double a0, double a1, double a2,
+                                               double a3, double* __restrict__ x,
+                                               double* __restrict__ v, double* __restrict__ p,
+                                               double* __restrict__ pval, int64_t ld,
+                                               const double* gX, double* blk_f,
+                                               long long* blk_i, unsigned* done, double* cand,
+                                               double* gX_out, double* gbest_out,
+                                               const PsoXchg* xg, unsigned long long seq) {
   using T = PsoTerms<Obj>;
   extern __shared__ double pso_tile_sm[];
   const int LP = pso_tile_log2(d), P = 1 << LP, PM = P - 1;
@@ -464,12 +473,20 @@ __global__ void __launch_bounds__(kPsoBlock)
     if (j < np) {
       const double r1 = rs[u], r2 = rs[(d << LP) + u];
       const int64_t o = (int64_t)k * ld + base + j;
-      const double xk = x[o], vk = v[o], pk = p[o], gk = gX[k];
-      const double nv = w * vk + c1 * r1 * (pk - xk) + c2 * r2 * (gk - xk);
-      const double nx = xk + nv;
-      v[o] = nv;
-      x[o] = nx;
-      xs[u] = nx;
+      if constexpr (INIT) {  // low + range * r, as uniform_draw
+        const double xk = a0 + a1 * r1;
+        x[o] = xk;
+        p[o] = xk;
+        v[o] = a2 + a3 * r2;
+        xs[u] = xk;
+      } else {
+        const double xk = x[o], vk = v[o], pk = p[o], gk = gX[k];
+        const double nv = a0 * vk + a1 * r1 * (pk - xk) + a2 * r2 * (gk - xk);
+        const double nx = xk + nv;
+        v[o] = nv;
+        x[o] = nx;
+        xs[u] = nx;
+      }
     }
   }
   __syncthreads();
@@ -499,11 +516,17 @@ __global__ void __launch_bounds__(kPsoBlock)
         for (int k = 0; k < d; ++k) acc.push(xs[(k << LP) + j]);
         f = acc.result(d);
       }
-      double best = pval[base + j];
-      if (f < best) {  // strict: ties keep the old personal best (pso.py:161)
+      double best;
+      if constexpr (INIT) {
         best = f;
         pval[base + j] = f;
-        imp = 1;
+      } else {
+        best = pval[base + j];
+        if (f < best) {  // strict: ties keep the old personal best (pso.py:161)
+          best = f;
+          pval[base + j] = f;
+          imp = 1;
+        }
       }
       bf = best;
       bi = i0 + base + j;
@@ -511,9 +534,11 @@ __global__ void __launch_bounds__(kPsoBlock)
     improved[j] = imp;
   }
   __syncthreads();
-  for (int u = threadIdx.x; u < (d << LP); u += kPsoBlock) {
-    const int j = u & PM, k = u >> LP;
-    if (improved[j]) p[(int64_t)k * ld + base + j] = xs[u];
+  if constexpr (!INIT) {
+    for (int u = threadIdx.x; u < (d << LP); u += kPsoBlock) {
+      const int j = u & PM, k = u >> LP;
+      if (improved[j]) p[(int64_t)k * ld + base + j] = xs[u];
+    }
   }
   block_argmin<kPsoBlock>(bf, bi);
   if (threadIdx.x == 0) {
@@ -524,6 +549,31 @@ __global__ void __launch_bounds__(kPsoBlock)
     __syncthreads();  // block_argmin's shared scratch is reused by the finalize
     fused_finalize(done, d, i0, p, ld, blk_f, blk_i, cand, gX_out, gbest_out, xg, seq);
   }
+}
+
+template <class Obj>
+__global__ void __launch_bounds__(kPsoBlock)
+    pso_sweep_tiled_kernel(int d, int64_t n, int64_t i0, uint64_t seed, uint64_t k0, double w,
+                           double c1, double c2, double* __restrict__ x,
+                           double* __restrict__ v, double* __restrict__ p,
+                           double* __restrict__ pval, int64_t ld, const double* gX,
+                           double* blk_f, long long* blk_i, unsigned* done, double* cand,
+                           double* gX_out, double* gbest_out, const PsoXchg* xg,
+                           unsigned long long seq) {
+  pso_tiled_body<Obj, false>(d, n, i0, seed, k0, w, c1, c2, 0.0, x, v, p, pval, ld, gX, blk_f,
+                             blk_i, done, cand, gX_out, gbest_out, xg, seq);
+}
+
+template <class Obj>
+__global__ void __launch_bounds__(kPsoBlock)
+    pso_init_tiled_kernel(int d, int64_t n, int64_t i0, uint64_t seed, double lower,
+                          double range, double vlow, double vrange, double* __restrict__ x,
+                          double* __restrict__ v, double* __restrict__ p,
+                          double* __restrict__ pval, int64_t ld, double* blk_f,
+                          long long* blk_i, unsigned* done, double* cand, double* gX_out,
+                          double* gbest_out, const PsoXchg* xg, unsigned long long seq) {
+  pso_tiled_body<Obj, true>(d, n, i0, seed, 0, lower, range, vlow, vrange, x, v, p, pval, ld,
+                            nullptr, blk_f, blk_i, done, cand, gX_out, gbest_out, xg, seq);
 }
 
 }  // namespace zeus

@@ -244,3 +244,31 @@ def test_update_swarm_from_fresh_streams(z):
         assert np.array_equal(state.positions[i], x[i] + vn), i
     # x = p = g: both attraction terms vanish (the reference's own check)
     assert np.allclose(state.velocities[gi], 0.5 * v[gi], atol=1e-15)
+
+
+@pytest.mark.parametrize("name,d,n", [("rastrigin", 20, 700), ("ackley", 40, 300)])
+def test_tiled_pso_wide_box_takes_the_libm_path(oracle, name, d, n):
+    """A box where |2 pi x| exceeds the branch-free reduction's range
+    (zeus_trig.cuh kTrigMax): the tiled kernels' term pass falls back to libm
+    per term.  Positions are pure arithmetic (bit-exact); values agree with
+    the oracle (glibc) to 1e-13."""
+    from paper_2603_28770_b200 import engine
+
+    lo, hi = -2.0e4, 2.0e4
+    dev = torch.device("cuda", 0)
+    sh = engine.SwarmShard(OBJ[name], d, n, 0, 7, dev)
+    sh.init(lo, hi)
+    x0 = sh.x.cpu().numpy().T.copy()
+    pv0 = sh.pval.cpu().numpy().copy()
+    ref = oracle.pso(name, d, n, 7, lo, hi, 0)
+    assert np.array_equal(x0, ref.positions)
+    assert np.max(np.abs(x0) * 2 * np.pi) > 1.0e5  # the fallback is exercised
+    rel = np.abs(pv0 - ref.personal_best_val) / np.maximum(1.0, np.abs(ref.personal_best_val))
+    assert rel.max() <= 1e-13
+    sh.select(sh.cand, 1)
+    sh.sweep(0.5, 1.2, 1.5)
+    ref1 = oracle.pso(name, d, n, 7, lo, hi, 1)
+    x1 = sh.x.cpu().numpy().T
+    assert np.array_equal(x1, ref1.positions)  # gX = the same argmin unless values tie
+    rel = np.abs(sh.pval.cpu().numpy() - ref1.personal_best_val)
+    assert (rel / np.maximum(1.0, np.abs(ref1.personal_best_val))).max() <= 1e-13

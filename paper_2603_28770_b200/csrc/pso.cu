@@ -31,9 +31,24 @@ static int launch_sweep(int d, int64_t n, int64_t i0, uint64_t seed, uint64_t k0
     (void)attr;
     const int P = 1 << pso_tile_log2(d);
     const int nb = n > 0 ? (int)((n + P - 1) / P) : 1;
-    pso_sweep_tiled_kernel<Obj><<<nb, kPsoBlock, pso_tile_smem(d), s>>>(
-        d, n, i0, seed, k0, w, c1, c2, x, v, p, pval, ld, gX, blk_f, blk_i, done, cand, gX_out,
-        gbest_out, xg, seq);
+    // programmatic dependent launch: this sweep's draw pass overlaps the tail
+    // of the previous PSO kernel on the stream (pso_tiled_body).  Not with a
+    // peer exchange: there the previous sweep's last CTA waits for the other
+    // ranks' sweeps, and ranks sharing a GPU (emulated shards, several
+    // processes on one device) would find SM slots held by CTAs of the next
+    // sweep waiting on that CTA -- measured: the 8-rank exchange test times out
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(nb);
+    lc.blockDim = dim3(kPsoBlock);
+    lc.dynamicSmemBytes = pso_tile_smem(d);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = xg ? 0 : 1;
+    cudaLaunchKernelEx(&lc, pso_sweep_tiled_kernel<Obj>, d, n, i0, seed, k0, w, c1, c2, x, v, p,
+                       pval, ld, gX, blk_f, blk_i, done, cand, gX_out, gbest_out, xg, seq);
     return nb;
   }
   const int nb = n > 0 ? (int)((n + kPsoBlock - 1) / kPsoBlock) : 1;

@@ -444,6 +444,12 @@ __device__ __forceinline__ void pso_tiled_body(int d, int64_t n, int64_t i0, uin
                                                double* gX_out, double* gbest_out,
                                                const PsoXchg* xg, unsigned long long seq) {
   using T = PsoTerms<Obj>;
+  // programmatic dependent launch (pso.cu launch_pso_tiled): the next sweep
+  // may be scheduled as soon as every CTA of this one is resident; it
+  // generates its draws (pass 1: no global reads) while this one finishes,
+  // then waits (griddepcontrol.wait: this grid complete, its writes visible)
+  // before touching the swarm.  Both are no-ops for an ordinary launch.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ double pso_tile_sm[];
   const int LP = pso_tile_log2(d), P = 1 << LP, PM = P - 1;
   double* rs = pso_tile_sm;     // [2d][P] uniform draws, then [NT d][P] terms
@@ -467,6 +473,7 @@ __device__ __forceinline__ void pso_tiled_body(int d, int64_t n, int64_t i0, uin
       }
     }
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   for (int u = threadIdx.x; u < (d << LP); u += kPsoBlock) {
     const int j = u & PM, k = u >> LP;
